@@ -1,0 +1,157 @@
+"""ctypes binding of the C ABI declared in include/wap_b200.h.
+
+This is the only door from Python into the sm_100a kernels. There is no CPU
+fallback: if the library is missing or CUDA is unavailable, every call raises
+(`NativeUnavailable`), so a GPU run can never silently degrade to host code.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+from .errors import EvalError, WorkloadError
+
+_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libwapb200.so"
+MAX_TAPS = 32
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA extension could not be loaded (no GPU path available)."""
+
+
+class wap_operand_t(C.Structure):
+    _fields_ = [
+        ("ptr", C.c_void_p),
+        ("inner", C.c_int64),
+        ("outer", C.c_int64),
+        ("ld", C.c_int64),
+        ("mn_major", C.c_int32),
+        ("tap_period", C.c_int32),
+        ("ntaps", C.c_int32),
+        ("off", C.c_int32 * MAX_TAPS),
+    ]
+
+
+class wap_gemm_desc_t(C.Structure):
+    _fields_ = [
+        ("M", C.c_int64),
+        ("N", C.c_int64),
+        ("K", C.c_int64),
+        ("a", wap_operand_t),
+        ("b", wap_operand_t),
+        ("c", C.c_void_p),
+        ("ldc", C.c_int64),
+        ("bias", C.c_void_p),
+        ("relu", C.c_int32),
+        ("mask", C.c_void_p),
+        ("ldm", C.c_int64),
+        ("halo_pad", C.c_int32),
+        ("halo_h", C.c_int32),
+        ("halo_w", C.c_int32),
+        ("precision", C.c_int32),
+        ("splits", C.c_int32),
+        ("block_n", C.c_int32),
+        ("workspace", C.c_void_p),
+        ("workspace_bytes", C.c_int64),
+    ]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load (once) and return the native library."""
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise NativeUnavailable(
+                f"{_LIB_PATH} not built; run `python -m paper_1811_01532_b200.build`"
+            )
+        _lib = C.CDLL(str(_LIB_PATH))
+        _declare(_lib)
+    return _lib
+
+
+def lib_path() -> Path:
+    return _LIB_PATH
+
+
+def _declare(L: C.CDLL) -> None:
+    for name, res, args in _SIGNATURES:
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+_P = C.c_void_p
+_I = C.c_int
+_I64 = C.c_int64
+_F = C.c_float
+_D = C.c_double
+
+# (name, restype, argtypes) for every symbol include/wap_b200.h declares.
+_SIGNATURES: list[tuple[str, object, list]] = [
+    ("wap_version", C.c_char_p, []),
+    ("wap_last_error", C.c_char_p, []),
+    ("wap_launch_count", C.c_longlong, []),
+    ("wap_gemm_workspace_bytes", _I64, [C.POINTER(wap_gemm_desc_t)]),
+    ("wap_gemm", _I, [C.POINTER(wap_gemm_desc_t), _P]),
+    ("wap_gemm_plan_create", _I, [C.POINTER(wap_gemm_desc_t), C.POINTER(_P)]),
+    ("wap_gemm_plan_run", _I, [_P, _P]),
+    ("wap_gemm_plan_destroy", None, [_P]),
+]
+
+
+def exported_symbols() -> list[str]:
+    return [s[0] for s in _SIGNATURES]
+
+
+def check(rc: int, what: str = "native call", exc: type = EvalError) -> None:
+    """Map a C status onto the reference exception hierarchy (errors.py)."""
+    if rc != 0:
+        msg = lib().wap_last_error().decode(errors="replace")
+        if rc == -1 and exc is EvalError:
+            exc = WorkloadError if "degree" in msg else EvalError
+        raise exc(f"{what} failed ({rc}): {msg}")
+
+
+def launch_count() -> int:
+    return int(lib().wap_launch_count())
+
+
+def version() -> str:
+    return lib().wap_version().decode()
+
+
+def stream_ptr(stream=None) -> int:
+    """cudaStream_t of a torch stream (current stream when None)."""
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def operand(t, inner: int, outer: int, ld: int, mn_major: bool, tap_period: int = 0,
+            offsets: tuple[int, ...] = (0,)) -> wap_operand_t:
+    if len(offsets) > MAX_TAPS:
+        raise ValueError(f"at most {MAX_TAPS} taps, got {len(offsets)}")
+    op = wap_operand_t()
+    op.ptr = t if isinstance(t, int) else t.data_ptr()
+    op.inner, op.outer, op.ld = inner, outer, ld
+    op.mn_major = 1 if mn_major else 0
+    op.tap_period = tap_period
+    op.ntaps = len(offsets)
+    for i, o in enumerate(offsets):
+        op.off[i] = int(o)
+    return op
+
+
+def ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t if isinstance(t, int) else t.data_ptr()
+
+
+os.environ.setdefault("CUDA_MODULE_LOADING", "LAZY")

@@ -1,0 +1,104 @@
+"""tcgen05 shifted-GEMM kernel vs fp64 references (GPU).
+
+Tolerances (normwise: max|a-b| / max|ref|): 3xTF32 is fp32-accurate (<1e-5 on
+these sizes); single-pass TF32 keeps 10 mantissa bits (<4e-3)."""
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_1811_01532_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+TOL = {1: 4e-3, 3: 1e-5}
+
+
+def dev(a, b):
+    a = a.double()
+    b = b.double()
+    return ((a - b).abs().max() / b.abs().max().clamp_min(1e-30)).item()
+
+
+@pytest.mark.parametrize("prec", [1, 3])
+@pytest.mark.parametrize("M,Nn,Kk", [(256, 384, 512), (128, 1000, 4096), (200, 72, 96), (37, 4096, 9216)])
+def test_fc_forward(cuda, prec, M, Nn, Kk):
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(M, Kk, device=cuda, generator=g)
+    w = torch.randn(Kk, Nn, device=cuda, generator=g)
+    bias = torch.randn(Nn, device=cuda, generator=g)
+    y = torch.empty(M, Nn, device=cuda)
+    K.gemm(x, w, y, a_mn=False, b_mn=True, M=M, Nn=Nn, K=Kk, bias=bias, relu=True, precision=prec)
+    torch.cuda.synchronize()
+    ref = torch.relu(x.double() @ w.double() + bias.double())
+    assert dev(y, ref) < TOL[prec]
+
+
+@pytest.mark.parametrize("prec", [1, 3])
+@pytest.mark.parametrize("block_n", [64, 128, 256])
+def test_fc_dx_kmajor(cuda, prec, block_n):
+    if prec == 3 and block_n == 256:
+        pytest.skip("BN=256 is TF32-only")
+    g = torch.Generator(device="cuda").manual_seed(1)
+    M, Nin, Nout = 128, 512, 320
+    dy = torch.randn(M, Nout, device=cuda, generator=g)
+    w = torch.randn(Nin, Nout, device=cuda, generator=g)
+    dx = torch.empty(M, Nin, device=cuda)
+    K.gemm(dy, w, dx, a_mn=False, b_mn=False, M=M, Nn=Nin, K=Nout, precision=prec, block_n=block_n)
+    torch.cuda.synchronize()
+    assert dev(dx, dy.double() @ w.double().T) < TOL[prec]
+
+
+@pytest.mark.parametrize("prec", [1, 3])
+@pytest.mark.parametrize("splits", [1, 3])
+def test_fc_dw_mnmajor(cuda, prec, splits):
+    g = torch.Generator(device="cuda").manual_seed(2)
+    Bt, Nin, Nout = 256, 384, 256
+    x = torch.randn(Bt, Nin, device=cuda, generator=g)
+    dy = torch.randn(Bt, Nout, device=cuda, generator=g)
+    dw = torch.empty(Nin, Nout, device=cuda)
+    K.gemm(x, dy, dw, a_mn=True, b_mn=True, M=Nin, Nn=Nout, K=Bt, precision=prec, splits=splits)
+    torch.cuda.synchronize()
+    assert dev(dw, x.double().T @ dy.double()) < TOL[prec]
+
+
+def _pad(x, p):
+    return F.pad(x, (0, 0, p, p, p, p)).contiguous()
+
+
+@pytest.mark.parametrize("prec", [1, 3])
+@pytest.mark.parametrize("Bn,H,Ci,Co,k", [(2, 13, 64, 128, 3), (2, 27, 64, 192, 5), (1, 14, 96, 64, 3)])
+def test_conv_shifted(cuda, prec, Bn, H, Ci, Co, k):
+    W = H
+    p = k // 2
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.relu(torch.randn(Bn, H, W, Ci, device=cuda, generator=g))
+    w = torch.randn(k, k, Ci, Co, device=cuda, generator=g) * 0.1
+    bias = torch.randn(Co, device=cuda, generator=g)
+    xp = _pad(x, p)
+    yp = torch.full((Bn, H + 2 * p, W + 2 * p, Co), float("nan"), device=cuda)
+    K.conv_fprop(xp, w, yp, B=Bn, H=H, W=W, Ci=Ci, Co=Co, k=k, pad=p, bias=bias, relu=True, precision=prec)
+    torch.cuda.synchronize()
+    ref = F.conv2d(x.double().permute(0, 3, 1, 2), w.double().permute(3, 2, 0, 1), bias.double(), padding=p)
+    ref = torch.relu(ref).permute(0, 2, 3, 1)
+    assert dev(yp[:, p:p + H, p:p + W], ref) < TOL[prec]
+    assert yp[:, :p].abs().max().item() == 0 and yp[:, :, :p].abs().max().item() == 0
+    assert yp[:, p + H:].abs().max().item() == 0 and yp[:, :, p + W:].abs().max().item() == 0
+
+    # dgrad with a fused ReLU mask, and wgrad
+    dy = torch.randn(Bn, H, W, Co, device=cuda, generator=g)
+    dyp = _pad(dy, p)
+    dxp = torch.full_like(xp, float("nan"))
+    K.conv_dgrad(dyp, w, dxp, B=Bn, H=H, W=W, Ci=Ci, Co=Co, k=k, pad=p, mask=xp, precision=prec)
+    dw = torch.empty_like(w)
+    K.conv_wgrad(xp, dyp, dw, B=Bn, H=H, W=W, Ci=Ci, Co=Co, k=k, pad=p, precision=prec)
+    torch.cuda.synchronize()
+    xd = x.double().permute(0, 3, 1, 2).requires_grad_(True)
+    wd = w.double().permute(3, 2, 0, 1).detach().requires_grad_(True)
+    out = F.conv2d(xd, wd, padding=p)
+    out.backward(dy.double().permute(0, 3, 1, 2))
+    ref_dx = (xd.grad * (xd > 0)).permute(0, 2, 3, 1)
+    ref_dw = wd.grad.permute(2, 3, 1, 0)
+    assert dev(dxp[:, p:p + H, p:p + W], ref_dx) < TOL[prec]
+    assert dxp[:, :p].abs().max().item() == 0
+    assert dev(dw, ref_dw) < TOL[prec]
