@@ -81,6 +81,88 @@ int wap_gemm_plan_create(const wap_gemm_desc_t* desc, void** plan);
 int wap_gemm_plan_run(void* plan, void* stream);
 void wap_gemm_plan_destroy(void* plan);
 
+/* ---- activation layout --------------------------------------------------- */
+/* Logical NHWC [B, H, W, C] stored as [B, H+2*pad, W+2*pad, ld] (ld >= C,
+ * ld % 4 == 0, halo rows zero). A 2D matrix [rows, cols] is B=rows, H=W=1,
+ * C=cols, pad=0. Element (b,h,w,c) lives at
+ *   ((b*(H+2p) + h+p)*(W+2p) + w+p)*ld + c. */
+typedef struct {
+  int32_t B, H, W, C;
+  int32_t pad;
+  int32_t ld;
+} wap_layout_t;
+
+/* im2col for Conv2D with any stride/padding (interp.py:69-79 generalised):
+ * col[(b,ho,wo), (u,v,c)] = x[b, ho*s+u-p, wo*s+v-p, c] (0 outside), columns
+ * K..ldcol-1 zeroed. `x` uses layout `xl`; col is [B*Ho*Wo, ldcol]. */
+int wap_im2col(const float* x, wap_layout_t xl, int k, int stride, int padding, int Ho, int Wo,
+               float* col, int64_t ldcol, void* stream);
+/* col2im (gather form, deterministic) for GradConv2DX (interp.py:94-102):
+ * dx[b,h,w,c] = sum over taps mapping to (h,w) of dcol[(b,ho,wo),(u,v,c)],
+ * optionally times [mask[b,h,w,c] > 0] (fused GradReLU, interp.py:197-198). */
+int wap_col2im(const float* dcol, int64_t ldcol, int k, int stride, int padding, int Ho, int Wo,
+               float* dx, wap_layout_t dxl, const float* mask, wap_layout_t ml, void* stream);
+
+/* Elementwise (interp.py:166-169,197-198): op 0 = BiasAdd y = x + b[c],
+ * 1 = ReLU y = max(x, 0), 2 = BiasAdd+ReLU, 3 = GradReLU y = dy * [x > 0]
+ * (x = second operand `aux`), 4 = copy / re-layout. */
+int wap_elementwise(int op, const float* x, wap_layout_t xl, const float* aux, wap_layout_t al,
+                    const float* bias, float* y, wap_layout_t yl, void* stream);
+/* AddN / AllReduceSum evaluated in one process (interp.py:115-119): left fold
+ * y = ((x0 + x1) + x2) + ... over n <= 16 inputs of identical layout. */
+int wap_add_n(const float* const* xs, int n, wap_layout_t l, float* y, void* stream);
+/* GradBias (interp.py:194-196): db[c] = sum over all rows of dy[..., c];
+ * deterministic two-pass reduction, `work` >= wap_bias_grad_work_floats(l) floats. */
+int64_t wap_bias_grad_work_floats(wap_layout_t l);
+int wap_bias_grad(const float* dy, wap_layout_t l, float* db, float* work, void* stream);
+/* MaxPool (VALID windows): forward writes y and the argmax position inside
+ * each window (uint8, indexed like y's storage; ties -> first maximum in
+ * row-major window order). Backward is a deterministic gather of dy through
+ * the stored argmax, optionally times [mask > 0] (fused GradReLU). */
+int wap_maxpool_fwd(const float* x, wap_layout_t xl, int window, int stride, float* y, wap_layout_t yl,
+                    uint8_t* argmax, void* stream);
+int wap_maxpool_bwd(const uint8_t* argmax, const float* dy, wap_layout_t dyl, int window, int stride,
+                    float* dx, wap_layout_t dxl, const float* mask, wap_layout_t ml, void* stream);
+/* LRN across channels: y = x / (bias + alpha * sum_{|j-c|<=size/2} x_j^2)^beta. */
+int wap_lrn_fwd(const float* x, wap_layout_t xl, int size, float alpha, float beta, float bias, float* y,
+                wap_layout_t yl, void* stream);
+int wap_lrn_bwd(const float* x, wap_layout_t xl, const float* dy, wap_layout_t dyl, int size, float alpha,
+                float beta, float bias, float* dx, wap_layout_t dxl, const float* mask, wap_layout_t ml,
+                void* stream);
+/* Fused SoftmaxXentLoss + GradSoftmaxXent (interp.py:170-175,199-202):
+ * loss[0] = sum_rows -(y . logsoftmax(z)) / rows; dz = (softmax(z) - y) / denominator.
+ * `work` holds `rows` floats (per-row losses, summed in row order). */
+int wap_xent_fwd_bwd(const float* logits, int64_t ldz, const float* labels, int64_t ldy, int rows, int cols,
+                     float denominator, float* loss, float* dlogits, int64_t ldd, float* work, void* stream);
+/* SgdUpdate (interp.py:203-204): w_out = w - lr * g over n contiguous floats
+ * (w_out may alias w: in-place update of the replicated variable). */
+int wap_sgd(const float* w, const float* g, float lr, float* w_out, int64_t n, void* stream);
+
+/* ---- Workload Analysis Unit on device (workloads.py:84-204, planner.py:151-246) */
+/* One primary layer as the parser sees it. kind 0 = MatMul ([batch, cin] x
+ * [cin, cout]), 1 = Conv2D (output [batch, out_h, out_w, cout], k x k kernel).
+ * n_grad = number of gradient companions present (1 for the first layer, else 2);
+ * weight_elems = weight + bias-of-BiasAdd elements (4 bytes each). */
+typedef struct {
+  int32_t kind;
+  int32_t n_grad;
+  int64_t batch, out_h, out_w, cin, cout, k;
+  int64_t weight_elems;
+} wap_wau_layer_t;
+
+typedef struct {
+  double peak_flops, efficiency_knee_flops, link_bandwidth, link_latency, allreduce_chunk_latency;
+} wap_wau_profile_t;
+
+/* Sweep d = 1..n_devices (candidates: d | global_batch), IEEE fp64 with no FMA
+ * contraction and CPython-3.12 compensated summation over layers, ties -> smaller d.
+ * All pointers are DEVICE pointers: layers[n_layers]; flops_out[2*n_layers]
+ * (fwd, bwd per layer); t_c/t_s/thr[n_devices] (NaN for non-candidates);
+ * d_out[1]. algo: 0 = ring, 1 = naive all-to-all. */
+int wap_wau_select(const wap_wau_layer_t* layers, int n_layers, int64_t global_batch, int n_devices,
+                   wap_wau_profile_t profile, int algo, int64_t* flops_out, double* t_c, double* t_s,
+                   double* thr, int32_t* d_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

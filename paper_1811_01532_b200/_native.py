@@ -58,6 +58,23 @@ class wap_gemm_desc_t(C.Structure):
     ]
 
 
+class wap_layout_t(C.Structure):
+    _fields_ = [("B", C.c_int32), ("H", C.c_int32), ("W", C.c_int32), ("C", C.c_int32),
+                ("pad", C.c_int32), ("ld", C.c_int32)]
+
+
+class wap_wau_layer_t(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n_grad", C.c_int32), ("batch", C.c_int64),
+                ("out_h", C.c_int64), ("out_w", C.c_int64), ("cin", C.c_int64),
+                ("cout", C.c_int64), ("k", C.c_int64), ("weight_elems", C.c_int64)]
+
+
+class wap_wau_profile_t(C.Structure):
+    _fields_ = [("peak_flops", C.c_double), ("efficiency_knee_flops", C.c_double),
+                ("link_bandwidth", C.c_double), ("link_latency", C.c_double),
+                ("allreduce_chunk_latency", C.c_double)]
+
+
 _lib = None
 
 
@@ -101,6 +118,21 @@ _SIGNATURES: list[tuple[str, object, list]] = [
     ("wap_gemm_plan_create", _I, [C.POINTER(wap_gemm_desc_t), C.POINTER(_P)]),
     ("wap_gemm_plan_run", _I, [_P, _P]),
     ("wap_gemm_plan_destroy", None, [_P]),
+    ("wap_im2col", _I, [_P, wap_layout_t, _I, _I, _I, _I, _I, _P, _I64, _P]),
+    ("wap_col2im", _I, [_P, _I64, _I, _I, _I, _I, _I, _P, wap_layout_t, _P, wap_layout_t, _P]),
+    ("wap_elementwise", _I, [_I, _P, wap_layout_t, _P, wap_layout_t, _P, _P, wap_layout_t, _P]),
+    ("wap_add_n", _I, [C.POINTER(_P), _I, wap_layout_t, _P, _P]),
+    ("wap_bias_grad_work_floats", _I64, [wap_layout_t]),
+    ("wap_bias_grad", _I, [_P, wap_layout_t, _P, _P, _P]),
+    ("wap_maxpool_fwd", _I, [_P, wap_layout_t, _I, _I, _P, wap_layout_t, _P, _P]),
+    ("wap_maxpool_bwd", _I, [_P, _P, wap_layout_t, _I, _I, _P, wap_layout_t, _P, wap_layout_t, _P]),
+    ("wap_lrn_fwd", _I, [_P, wap_layout_t, _I, _F, _F, _F, _P, wap_layout_t, _P]),
+    ("wap_lrn_bwd", _I, [_P, wap_layout_t, _P, wap_layout_t, _I, _F, _F, _F, _P, wap_layout_t, _P,
+                         wap_layout_t, _P]),
+    ("wap_xent_fwd_bwd", _I, [_P, _I64, _P, _I64, _I, _I, _F, _P, _P, _I64, _P, _P]),
+    ("wap_sgd", _I, [_P, _P, _F, _P, _I64, _P]),
+    ("wap_wau_select", _I, [C.POINTER(wap_wau_layer_t), _I, _I64, _I, wap_wau_profile_t, _I, _P, _P,
+                            _P, _P, _P, _P]),
 ]
 
 

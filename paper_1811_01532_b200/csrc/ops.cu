@@ -1,0 +1,625 @@
+// Memory-bound kernels of the WAP step: layout moves, im2col/col2im, elementwise
+// (BiasAdd/ReLU/GradReLU), AddN, GradBias, MaxPool, LRN, softmax-xent, SGD.
+// All are HBM-bound: coalesced along the contiguous channel axis, float4 where
+// the layout allows (ld % 4 == 0 always), grid = multiple of the 148 SMs,
+// reductions deterministic (fixed order, no atomics) so replicas stay bitwise equal.
+#include <atomic>
+
+#include "common.cuh"
+#include "../../include/wap_b200.h"
+
+extern std::atomic<long long> g_wap_launches;
+
+namespace {
+
+__host__ __device__ __forceinline__ int64_t lidx(const wap_layout_t& l, int b, int h, int w, int c) {
+  return (((int64_t)b * (l.H + 2 * l.pad) + h + l.pad) * (l.W + 2 * l.pad) + w + l.pad) * l.ld + c;
+}
+
+int grid_for(int64_t work, int threads) {
+  int64_t blocks = (work + threads - 1) / threads;
+  const int64_t cap = (int64_t)WAP_NUM_SMS * 16;
+  if (blocks > cap) blocks = cap;
+  return (int)(blocks < 1 ? 1 : blocks);
+}
+
+#define COUNT_LAUNCH() g_wap_launches.fetch_add(1, std::memory_order_relaxed)
+
+int check_layout(const wap_layout_t& l, const char* name) {
+  WAP_CHECK_ARG(l.B >= 1 && l.H >= 1 && l.W >= 1 && l.C >= 1, "%s: bad dims", name);
+  WAP_CHECK_ARG(l.pad >= 0, "%s: negative pad", name);
+  WAP_CHECK_ARG(l.ld >= l.C && l.ld % 4 == 0, "%s: ld=%d must be >= C=%d and a multiple of 4", name, l.ld, l.C);
+  return WAP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// elementwise: one thread per (pixel, 4 channels); lanes >= C written as 0
+// ---------------------------------------------------------------------------
+template <int OP>
+__global__ void elementwise_kernel(const float* __restrict__ x, wap_layout_t xl, const float* __restrict__ aux,
+                                   wap_layout_t al, const float* __restrict__ bias, float* __restrict__ y,
+                                   wap_layout_t yl) {
+  const int c4n = yl.ld / 4;
+  const int64_t total = (int64_t)yl.B * yl.H * yl.W * c4n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % c4n) * 4;
+    int64_t p = i / c4n;
+    const int w = (int)(p % yl.W);
+    p /= yl.W;
+    const int h = (int)(p % yl.H);
+    const int b = (int)(p / yl.H);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c < xl.ld) v = *reinterpret_cast<const float4*>(x + lidx(xl, b, h, w, c));
+    float o[4] = {v.x, v.y, v.z, v.w};
+    float m[4] = {1.f, 1.f, 1.f, 1.f};
+    if (OP == 3) {
+      const float4 a = *reinterpret_cast<const float4*>(aux + lidx(al, b, h, w, c));
+      m[0] = a.x; m[1] = a.y; m[2] = a.z; m[3] = a.w;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cc = c + j;
+      if (cc >= yl.C) { o[j] = 0.f; continue; }
+      if (OP == 0 || OP == 2) o[j] += __ldg(bias + cc);
+      if (OP == 1 || OP == 2) o[j] = fmaxf(o[j], 0.f);
+      if (OP == 3) o[j] = m[j] > 0.f ? o[j] : 0.f;
+    }
+    *reinterpret_cast<float4*>(y + lidx(yl, b, h, w, c)) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+struct PtrPack {
+  const float* p[16];
+};
+__global__ void add_n_kernel_packed(PtrPack xs, int n, float* __restrict__ y, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 acc = reinterpret_cast<const float4*>(xs.p[0])[i];
+    for (int k = 1; k < n; ++k) {
+      const float4 v = reinterpret_cast<const float4*>(xs.p[k])[i];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(y)[i] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GradBias: column sums, pass 1 = per-chunk partials, pass 2 = ordered sum
+// ---------------------------------------------------------------------------
+__global__ void bias_grad_partial(const float* __restrict__ dy, int64_t rows, int ld, int C, int64_t rows_per_chunk,
+                                  float* __restrict__ part) {
+  __shared__ float red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
+  const int chunk = blockIdx.y;
+  const int64_t r0 = chunk * rows_per_chunk;
+  const int64_t r1 = min(rows, r0 + rows_per_chunk);
+  float s = 0.f;
+  if (c < C)
+    for (int64_t r = r0 + ty; r < r1; r += 8) s += dy[r * ld + c];
+  red[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0) {
+    float t = red[0][tx];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) t += red[k][tx];
+    if (c < C) part[(int64_t)chunk * ld + c] = t;
+  }
+}
+
+__global__ void bias_grad_final(const float* __restrict__ part, int chunks, int ld, int C, float* __restrict__ db) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  float s = 0.f;
+  for (int k = 0; k < chunks; ++k) s += part[(int64_t)k * ld + c];
+  db[c] = s;
+}
+
+int bias_chunks(const wap_layout_t& l) {
+  const int64_t rows = (int64_t)l.B * (l.H + 2 * l.pad) * (l.W + 2 * l.pad);
+  const int ctiles = (l.C + 31) / 32;
+  int64_t chunks = (2 * WAP_NUM_SMS + ctiles - 1) / ctiles;
+  const int64_t max_chunks = (rows + 63) / 64;
+  if (chunks > max_chunks) chunks = max_chunks;
+  if (chunks < 1) chunks = 1;
+  return (int)chunks;
+}
+
+// ---------------------------------------------------------------------------
+// im2col / col2im
+// ---------------------------------------------------------------------------
+__global__ void im2col_kernel(const float* __restrict__ x, wap_layout_t xl, int k, int s, int p, int Ho, int Wo,
+                              float* __restrict__ col, int64_t ldcol) {
+  const int C = xl.C;
+  const int K = k * k * C;
+  const int64_t M = (int64_t)xl.B * Ho * Wo;
+  const int64_t total = M * ldcol;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int kk = (int)(i % ldcol);
+    const int64_t m = i / ldcol;
+    float v = 0.f;
+    if (kk < K) {
+      const int c = kk % C;
+      const int t = kk / C;
+      const int u = t / k, vv = t % k;
+      const int wo = (int)(m % Wo);
+      const int64_t r = m / Wo;
+      const int ho = (int)(r % Ho);
+      const int b = (int)(r / Ho);
+      const int hi = ho * s + u - p, wi = wo * s + vv - p;
+      if (hi >= 0 && hi < xl.H && wi >= 0 && wi < xl.W) v = __ldg(x + lidx(xl, b, hi, wi, c));
+    }
+    col[i] = v;
+  }
+}
+
+__global__ void col2im_kernel(const float* __restrict__ dcol, int64_t ldcol, int k, int s, int p, int Ho, int Wo,
+                              float* __restrict__ dx, wap_layout_t dl, const float* __restrict__ mask,
+                              wap_layout_t ml) {
+  const int C = dl.C;
+  const int64_t total = (int64_t)dl.B * dl.H * dl.W * dl.ld;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % dl.ld);
+    int64_t q = i / dl.ld;
+    const int w = (int)(q % dl.W);
+    q /= dl.W;
+    const int h = (int)(q % dl.H);
+    const int b = (int)(q / dl.H);
+    float acc = 0.f;
+    if (c < C) {
+      for (int u = 0; u < k; ++u) {
+        const int hs = h + p - u;
+        if (hs < 0 || hs % s) continue;
+        const int ho = hs / s;
+        if (ho >= Ho) continue;
+        for (int v = 0; v < k; ++v) {
+          const int ws = w + p - v;
+          if (ws < 0 || ws % s) continue;
+          const int wo = ws / s;
+          if (wo >= Wo) continue;
+          acc += dcol[(((int64_t)b * Ho + ho) * Wo + wo) * ldcol + (u * k + v) * C + c];
+        }
+      }
+      if (mask && !(mask[lidx(ml, b, h, w, c)] > 0.f)) acc = 0.f;
+    }
+    dx[lidx(dl, b, h, w, c)] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// MaxPool
+// ---------------------------------------------------------------------------
+__global__ void maxpool_fwd_kernel(const float* __restrict__ x, wap_layout_t xl, int win, int s,
+                                   float* __restrict__ y, wap_layout_t yl, uint8_t* __restrict__ arg) {
+  const int c4n = yl.ld / 4;
+  const int64_t total = (int64_t)yl.B * yl.H * yl.W * c4n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % c4n) * 4;
+    int64_t q = i / c4n;
+    const int wo = (int)(q % yl.W);
+    q /= yl.W;
+    const int ho = (int)(q % yl.H);
+    const int b = (int)(q / yl.H);
+    float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    int bi[4] = {0, 0, 0, 0};
+    for (int a = 0; a < win; ++a)
+      for (int bb = 0; bb < win; ++bb) {
+        const float4 v = *reinterpret_cast<const float4*>(x + lidx(xl, b, ho * s + a, wo * s + bb, c));
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (vv[j] > best[j]) { best[j] = vv[j]; bi[j] = a * win + bb; }
+      }
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = (c + j < yl.C) ? best[j] : 0.f;
+    const int64_t yi = lidx(yl, b, ho, wo, c);
+    *reinterpret_cast<float4*>(y + yi) = make_float4(o[0], o[1], o[2], o[3]);
+    if (arg) {
+      uchar4 a4 = make_uchar4((uint8_t)bi[0], (uint8_t)bi[1], (uint8_t)bi[2], (uint8_t)bi[3]);
+      *reinterpret_cast<uchar4*>(arg + yi) = a4;
+    }
+  }
+}
+
+__global__ void maxpool_bwd_kernel(const uint8_t* __restrict__ arg, const float* __restrict__ dy, wap_layout_t yl,
+                                   int win, int s, float* __restrict__ dx, wap_layout_t xl,
+                                   const float* __restrict__ mask, wap_layout_t ml) {
+  const int c4n = xl.ld / 4;
+  const int64_t total = (int64_t)xl.B * xl.H * xl.W * c4n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % c4n) * 4;
+    int64_t q = i / c4n;
+    const int w = (int)(q % xl.W);
+    q /= xl.W;
+    const int h = (int)(q % xl.H);
+    const int b = (int)(q / xl.H);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    // windows (ho, wo) with ho*s <= h < ho*s + win
+    const int ho_lo = h >= win ? (h - win) / s + 1 : 0;
+    const int ho_hi = min(h / s, yl.H - 1);
+    const int wo_lo = w >= win ? (w - win) / s + 1 : 0;
+    const int wo_hi = min(w / s, yl.W - 1);
+    for (int ho = ho_lo; ho <= ho_hi; ++ho)
+      for (int wo = wo_lo; wo <= wo_hi; ++wo) {
+        const int local = (h - ho * s) * win + (w - wo * s);
+        const int64_t yi = lidx(yl, b, ho, wo, c);
+        const uchar4 a = *reinterpret_cast<const uchar4*>(arg + yi);
+        const float4 g = *reinterpret_cast<const float4*>(dy + yi);
+        if (a.x == local) acc[0] += g.x;
+        if (a.y == local) acc[1] += g.y;
+        if (a.z == local) acc[2] += g.z;
+        if (a.w == local) acc[3] += g.w;
+      }
+    if (mask) {
+      const float4 m = *reinterpret_cast<const float4*>(mask + lidx(ml, b, h, w, c));
+      if (!(m.x > 0.f)) acc[0] = 0.f;
+      if (!(m.y > 0.f)) acc[1] = 0.f;
+      if (!(m.z > 0.f)) acc[2] = 0.f;
+      if (!(m.w > 0.f)) acc[3] = 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (c + j >= xl.C) acc[j] = 0.f;
+    *reinterpret_cast<float4*>(dx + lidx(xl, b, h, w, c)) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// LRN: a block handles PIX pixels; channels staged in shared memory
+// ---------------------------------------------------------------------------
+constexpr int LRN_PIX = 8;
+
+__device__ __forceinline__ void pixel_of(const wap_layout_t& l, int64_t p, int& b, int& h, int& w) {
+  w = (int)(p % l.W);
+  p /= l.W;
+  h = (int)(p % l.H);
+  b = (int)(p / l.H);
+}
+
+__global__ void lrn_fwd_kernel(const float* __restrict__ x, wap_layout_t xl, int size, float alpha, float beta,
+                               float k, float* __restrict__ y, wap_layout_t yl) {
+  extern __shared__ float sx[];  // [LRN_PIX][C]
+  const int C = xl.C;
+  const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
+  const int half = size / 2;
+  for (int64_t p0 = (int64_t)blockIdx.x * LRN_PIX; p0 < npix; p0 += (int64_t)gridDim.x * LRN_PIX) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < LRN_PIX * C; t += blockDim.x) {
+      const int pi = t / C, c = t % C;
+      const int64_t p = p0 + pi;
+      float v = 0.f;
+      if (p < npix) {
+        int b, h, w;
+        pixel_of(xl, p, b, h, w);
+        v = x[lidx(xl, b, h, w, c)];
+      }
+      sx[t] = v;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < LRN_PIX * yl.ld; t += blockDim.x) {
+      const int pi = t / yl.ld, c = t % yl.ld;
+      const int64_t p = p0 + pi;
+      if (p >= npix) continue;
+      int b, h, w;
+      pixel_of(yl, p, b, h, w);
+      float out = 0.f;
+      if (c < C) {
+        float ss = 0.f;
+        const int lo = max(0, c - half), hi = min(C - 1, c + half);
+        for (int j = lo; j <= hi; ++j) ss += sx[pi * C + j] * sx[pi * C + j];
+        out = sx[pi * C + c] * powf(k + alpha * ss, -beta);
+      }
+      y[lidx(yl, b, h, w, c)] = out;
+    }
+  }
+}
+
+__global__ void lrn_bwd_kernel(const float* __restrict__ x, wap_layout_t xl, const float* __restrict__ dy,
+                               wap_layout_t dyl, int size, float alpha, float beta, float k, float* __restrict__ dx,
+                               wap_layout_t dxl, const float* __restrict__ mask, wap_layout_t ml) {
+  extern __shared__ float sh[];  // x, dy, t (= dy*x*s^(-beta-1)), pw (= s^-beta): 4 * [LRN_PIX][C]
+  const int C = xl.C;
+  float* sx = sh;
+  float* sd = sh + LRN_PIX * C;
+  float* st = sh + 2 * LRN_PIX * C;
+  float* sp = sh + 3 * LRN_PIX * C;
+  const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
+  const int half = size / 2;
+  for (int64_t p0 = (int64_t)blockIdx.x * LRN_PIX; p0 < npix; p0 += (int64_t)gridDim.x * LRN_PIX) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < LRN_PIX * C; t += blockDim.x) {
+      const int pi = t / C, c = t % C;
+      const int64_t p = p0 + pi;
+      float vx = 0.f, vd = 0.f;
+      if (p < npix) {
+        int b, h, w;
+        pixel_of(xl, p, b, h, w);
+        vx = x[lidx(xl, b, h, w, c)];
+        vd = dy[lidx(dyl, b, h, w, c)];
+      }
+      sx[t] = vx;
+      sd[t] = vd;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < LRN_PIX * C; t += blockDim.x) {
+      const int pi = t / C, c = t % C;
+      float ss = 0.f;
+      const int lo = max(0, c - half), hi = min(C - 1, c + half);
+      for (int j = lo; j <= hi; ++j) ss += sx[pi * C + j] * sx[pi * C + j];
+      const float s = k + alpha * ss;
+      const float pw = powf(s, -beta);
+      sp[t] = pw;
+      st[t] = sd[t] * sx[t] * pw / s;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < LRN_PIX * dxl.ld; t += blockDim.x) {
+      const int pi = t / dxl.ld, c = t % dxl.ld;
+      const int64_t p = p0 + pi;
+      if (p >= npix) continue;
+      int b, h, w;
+      pixel_of(dxl, p, b, h, w);
+      float out = 0.f;
+      if (c < C) {
+        float acc = 0.f;
+        const int lo = max(0, c - half), hi = min(C - 1, c + half);
+        for (int j = lo; j <= hi; ++j) acc += st[pi * C + j];
+        out = sd[pi * C + c] * sp[pi * C + c] - 2.f * alpha * beta * sx[pi * C + c] * acc;
+        if (mask && !(mask[lidx(ml, b, h, w, c)] > 0.f)) out = 0.f;
+      }
+      dx[lidx(dxl, b, h, w, c)] = out;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// softmax cross-entropy (+ gradient): one block per row
+// ---------------------------------------------------------------------------
+__global__ void xent_row_kernel(const float* __restrict__ z, int64_t ldz, const float* __restrict__ y, int64_t ldy,
+                                int cols, float inv_denom, float* __restrict__ dz, int64_t ldd,
+                                float* __restrict__ row_loss) {
+  __shared__ float red[32];
+  const int r = blockIdx.x;
+  const float* zr = z + r * ldz;
+  const float* yr = y + r * ldy;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float mx = -INFINITY;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) mx = fmaxf(mx, zr[c]);
+  mx = warp_max(mx);
+  if (lane == 0) red[wid] = mx;
+  __syncthreads();
+  if (wid == 0) {
+    float v = lane < nw ? red[lane] : -INFINITY;
+    v = warp_max(v);
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  mx = red[0];
+  __syncthreads();
+  float se = 0.f;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) se += expf(zr[c] - mx);
+  se = warp_sum(se);
+  if (lane == 0) red[wid] = se;
+  __syncthreads();
+  if (wid == 0) {
+    float v = lane < nw ? red[lane] : 0.f;
+    v = warp_sum(v);
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  se = red[0];
+  __syncthreads();
+  const float lse = logf(se);
+  float l = 0.f;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    const float zc = zr[c] - mx;
+    const float yc = yr[c];
+    l -= yc * (zc - lse);
+    dz[r * ldd + c] = (expf(zc) / se - yc) * inv_denom;
+  }
+  l = warp_sum(l);
+  if (lane == 0) red[wid] = l;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float v = 0.f;
+    for (int k2 = 0; k2 < nw; ++k2) v += red[k2];
+    row_loss[r] = v;
+  }
+}
+
+__global__ void xent_final_kernel(const float* __restrict__ row_loss, int rows, float* __restrict__ loss) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int r = 0; r < rows; ++r) s += row_loss[r];
+    loss[0] = (float)(s / rows);
+  }
+}
+
+__global__ void sgd_kernel(const float* __restrict__ w, const float* __restrict__ g, float lr, float* __restrict__ o,
+                           int64_t n) {
+  const int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = reinterpret_cast<const float4*>(w)[i];
+    const float4 b = reinterpret_cast<const float4*>(g)[i];
+    reinterpret_cast<float4*>(o)[i] = make_float4(a.x - lr * b.x, a.y - lr * b.y, a.z - lr * b.z, a.w - lr * b.w);
+  }
+  for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = w[i] - lr * g[i];
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+#define STREAM(s) reinterpret_cast<cudaStream_t>(s)
+
+extern "C" int wap_elementwise(int op, const float* x, wap_layout_t xl, const float* aux, wap_layout_t al,
+                               const float* bias, float* y, wap_layout_t yl, void* stream) {
+  int rc;
+  if ((rc = check_layout(xl, "x")) || (rc = check_layout(yl, "y"))) return rc;
+  WAP_CHECK_ARG(x && y, "null pointer");
+  WAP_CHECK_ARG(xl.B == yl.B && xl.H == yl.H && xl.W == yl.W && xl.C == yl.C, "elementwise: shape mismatch");
+  if (op == 3) {
+    if ((rc = check_layout(al, "aux"))) return rc;
+    WAP_CHECK_ARG(aux != nullptr, "GradReLU needs the activation operand");
+  }
+  if (op == 0 || op == 2) WAP_CHECK_ARG(bias != nullptr, "BiasAdd needs a bias");
+  const int threads = 256;
+  const int64_t work = (int64_t)yl.B * yl.H * yl.W * (yl.ld / 4);
+  const int blocks = grid_for(work, threads);
+  switch (op) {
+    case 0: elementwise_kernel<0><<<blocks, threads, 0, STREAM(stream)>>>(x, xl, aux, al, bias, y, yl); break;
+    case 1: elementwise_kernel<1><<<blocks, threads, 0, STREAM(stream)>>>(x, xl, aux, al, bias, y, yl); break;
+    case 2: elementwise_kernel<2><<<blocks, threads, 0, STREAM(stream)>>>(x, xl, aux, al, bias, y, yl); break;
+    case 3: elementwise_kernel<3><<<blocks, threads, 0, STREAM(stream)>>>(x, xl, aux, al, bias, y, yl); break;
+    case 4: elementwise_kernel<4><<<blocks, threads, 0, STREAM(stream)>>>(x, xl, aux, al, bias, y, yl); break;
+    default: WAP_CHECK_ARG(false, "unknown elementwise op %d", op);
+  }
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
+  return WAP_OK;
+}
+
+extern "C" int wap_add_n(const float* const* xs, int n, wap_layout_t l, float* y, void* stream) {
+  int rc;
+  if ((rc = check_layout(l, "x"))) return rc;
+  WAP_CHECK_ARG(n >= 1 && n <= 16, "add_n supports 1..16 operands, got %d", n);
+  PtrPack pk;
+  for (int i = 0; i < n; ++i) {
+    WAP_CHECK_ARG(xs[i] != nullptr, "null operand %d", i);
+    pk.p[i] = xs[i];
+  }
+  const int64_t n4 = (int64_t)l.B * (l.H + 2 * l.pad) * (l.W + 2 * l.pad) * l.ld / 4;
+  add_n_kernel_packed<<<grid_for(n4, 256), 256, 0, STREAM(stream)>>>(pk, n, y, n4);
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
+  return WAP_OK;
+}
+
+extern "C" int64_t wap_bias_grad_work_floats(wap_layout_t l) { return (int64_t)bias_chunks(l) * l.ld; }
+
+extern "C" int wap_bias_grad(const float* dy, wap_layout_t l, float* db, float* work, void* stream) {
+  int rc;
+  if ((rc = check_layout(l, "dy"))) return rc;
+  WAP_CHECK_ARG(dy && db && work, "null pointer");
+  const int64_t rows = (int64_t)l.B * (l.H + 2 * l.pad) * (l.W + 2 * l.pad);
+  const int chunks = bias_chunks(l);
+  const int64_t rpc = (rows + chunks - 1) / chunks;
+  dim3 grid((l.C + 31) / 32, chunks);
+  bias_grad_partial<<<grid, 256, 0, STREAM(stream)>>>(dy, rows, l.ld, l.C, rpc, work);
+  WAP_LAUNCH_CHECK();
+  bias_grad_final<<<(l.C + 127) / 128, 128, 0, STREAM(stream)>>>(work, chunks, l.ld, l.C, db);
+  WAP_LAUNCH_CHECK();
+  g_wap_launches.fetch_add(2, std::memory_order_relaxed);
+  return WAP_OK;
+}
+
+extern "C" int wap_im2col(const float* x, wap_layout_t xl, int k, int stride, int padding, int Ho, int Wo,
+                          float* col, int64_t ldcol, void* stream) {
+  int rc;
+  if ((rc = check_layout(xl, "x"))) return rc;
+  WAP_CHECK_ARG(k >= 1 && stride >= 1 && padding >= 0 && Ho >= 1 && Wo >= 1, "im2col: bad geometry");
+  WAP_CHECK_ARG(ldcol >= (int64_t)k * k * xl.C, "im2col: ldcol too small");
+  const int64_t total = (int64_t)xl.B * Ho * Wo * ldcol;
+  im2col_kernel<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(x, xl, k, stride, padding, Ho, Wo, col, ldcol);
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
+  return WAP_OK;
+}
+
+extern "C" int wap_col2im(const float* dcol, int64_t ldcol, int k, int stride, int padding, int Ho, int Wo,
+                          float* dx, wap_layout_t dxl, const float* mask, wap_layout_t ml, void* stream) {
+  int rc;
+  if ((rc = check_layout(dxl, "dx"))) return rc;
+  if (mask && (rc = check_layout(ml, "mask"))) return rc;
+  WAP_CHECK_ARG(ldcol >= (int64_t)k * k * dxl.C, "col2im: ldcol too small");
+  const int64_t total = (int64_t)dxl.B * dxl.H * dxl.W * dxl.ld;
+  col2im_kernel<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(dcol, ldcol, k, stride, padding, Ho, Wo, dx, dxl,
+                                                                 mask, ml);
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
+  return WAP_OK;
+}
+
+extern "C" int wap_maxpool_fwd(const float* x, wap_layout_t xl, int window, int stride, float* y, wap_layout_t yl,
+                               uint8_t* argmax, void* stream) {
+  int rc;
+  if ((rc = check_layout(xl, "x")) || (rc = check_layout(yl, "y"))) return rc;
+  WAP_CHECK_ARG(window >= 1 && window <= 15 && stride >= 1, "maxpool: bad window/stride");
+  WAP_CHECK_ARG(yl.H == (xl.H - window) / stride + 1 && yl.W == (xl.W - window) / stride + 1 && yl.C == xl.C &&
+                    yl.B == xl.B && xl.ld == yl.ld,
+                "maxpool: output layout does not match");
+  const int64_t work = (int64_t)yl.B * yl.H * yl.W * (yl.ld / 4);
+  maxpool_fwd_kernel<<<grid_for(work, 256), 256, 0, STREAM(stream)>>>(x, xl, window, stride, y, yl, argmax);
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
+  return WAP_OK;
+}
+
+extern "C" int wap_maxpool_bwd(const uint8_t* argmax, const float* dy, wap_layout_t dyl, int window, int stride,
+                               float* dx, wap_layout_t dxl, const float* mask, wap_layout_t ml, void* stream) {
+  int rc;
+  if ((rc = check_layout(dyl, "dy")) || (rc = check_layout(dxl, "dx"))) return rc;
+  if (mask && (rc = check_layout(ml, "mask"))) return rc;
+  WAP_CHECK_ARG(argmax != nullptr, "maxpool backward needs the forward argmax");
+  WAP_CHECK_ARG(dxl.ld == dyl.ld, "maxpool: dx/dy ld mismatch");
+  const int64_t work = (int64_t)dxl.B * dxl.H * dxl.W * (dxl.ld / 4);
+  maxpool_bwd_kernel<<<grid_for(work, 256), 256, 0, STREAM(stream)>>>(argmax, dy, dyl, window, stride, dx, dxl, mask,
+                                                                     ml);
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
+  return WAP_OK;
+}
+
+extern "C" int wap_lrn_fwd(const float* x, wap_layout_t xl, int size, float alpha, float beta, float bias, float* y,
+                           wap_layout_t yl, void* stream) {
+  int rc;
+  if ((rc = check_layout(xl, "x")) || (rc = check_layout(yl, "y"))) return rc;
+  WAP_CHECK_ARG(size >= 1 && size % 2 == 1, "LRN size must be odd");
+  const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
+  const int smem = LRN_PIX * xl.C * 4;
+  lrn_fwd_kernel<<<grid_for(npix, LRN_PIX), 256, smem, STREAM(stream)>>>(x, xl, size, alpha, beta, bias, y, yl);
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
+  return WAP_OK;
+}
+
+extern "C" int wap_lrn_bwd(const float* x, wap_layout_t xl, const float* dy, wap_layout_t dyl, int size, float alpha,
+                           float beta, float bias, float* dx, wap_layout_t dxl, const float* mask, wap_layout_t ml,
+                           void* stream) {
+  int rc;
+  if ((rc = check_layout(xl, "x")) || (rc = check_layout(dyl, "dy")) || (rc = check_layout(dxl, "dx"))) return rc;
+  if (mask && (rc = check_layout(ml, "mask"))) return rc;
+  const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
+  const int smem = 4 * LRN_PIX * xl.C * 4;
+  lrn_bwd_kernel<<<grid_for(npix, LRN_PIX), 256, smem, STREAM(stream)>>>(x, xl, dy, dyl, size, alpha, beta, bias,
+                                                                         dx, dxl, mask, ml);
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
+  return WAP_OK;
+}
+
+extern "C" int wap_xent_fwd_bwd(const float* logits, int64_t ldz, const float* labels, int64_t ldy, int rows,
+                                int cols, float denominator, float* loss, float* dlogits, int64_t ldd, float* work,
+                                void* stream) {
+  WAP_CHECK_ARG(logits && labels && loss && dlogits && work, "null pointer");
+  WAP_CHECK_ARG(rows >= 1 && cols >= 1 && denominator >= 1.f, "xent: bad shape/denominator");
+  xent_row_kernel<<<rows, 256, 0, STREAM(stream)>>>(logits, ldz, labels, ldy, cols, 1.f / denominator, dlogits, ldd,
+                                                    work);
+  WAP_LAUNCH_CHECK();
+  xent_final_kernel<<<1, 32, 0, STREAM(stream)>>>(work, rows, loss);
+  WAP_LAUNCH_CHECK();
+  g_wap_launches.fetch_add(2, std::memory_order_relaxed);
+  return WAP_OK;
+}
+
+extern "C" int wap_sgd(const float* w, const float* g, float lr, float* w_out, int64_t n, void* stream) {
+  WAP_CHECK_ARG(w && g && w_out && n >= 0, "sgd: bad arguments");
+  WAP_CHECK_ARG(((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(w_out)) & 15) == 0,
+                "sgd: buffers must be 16-byte aligned");
+  if (n == 0) return WAP_OK;
+  sgd_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, STREAM(stream)>>>(w, g, lr, w_out, n);
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
+  return WAP_OK;
+}
