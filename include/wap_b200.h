@@ -94,13 +94,15 @@ typedef struct {
 
 /* im2col for Conv2D with any stride/padding (interp.py:69-79 generalised):
  * col[(b,ho,wo), (u,v,c)] = x[b, ho*s+u-p, wo*s+v-p, c] (0 outside), columns
- * K..ldcol-1 zeroed. `x` uses layout `xl`; col is [B*Ho*Wo, ldcol]. */
-int wap_im2col(const float* x, wap_layout_t xl, int k, int stride, int padding, int Ho, int Wo,
+ * K..ldcol-1 zeroed. Rows enumerate the output grid padded by out_pad (halo
+ * rows zero): col is [B*(Ho+2*out_pad)*(Wo+2*out_pad), ldcol]. */
+int wap_im2col(const float* x, wap_layout_t xl, int k, int stride, int padding, int Ho, int Wo, int out_pad,
                float* col, int64_t ldcol, void* stream);
 /* col2im (gather form, deterministic) for GradConv2DX (interp.py:94-102):
- * dx[b,h,w,c] = sum over taps mapping to (h,w) of dcol[(b,ho,wo),(u,v,c)],
- * optionally times [mask[b,h,w,c] > 0] (fused GradReLU, interp.py:197-198). */
-int wap_col2im(const float* dcol, int64_t ldcol, int k, int stride, int padding, int Ho, int Wo,
+ * dx[b,h,w,c] = sum over taps mapping to (h,w) of dcol[(b,ho,wo),(u,v,c)]
+ * (dcol rows on the out_pad-padded output grid), optionally times
+ * [mask[b,h,w,c] > 0] (fused GradReLU, interp.py:197-198). */
+int wap_col2im(const float* dcol, int64_t ldcol, int k, int stride, int padding, int Ho, int Wo, int out_pad,
                float* dx, wap_layout_t dxl, const float* mask, wap_layout_t ml, void* stream);
 
 /* Elementwise (interp.py:166-169,197-198): op 0 = BiasAdd y = x + b[c],
@@ -134,6 +136,10 @@ int wap_lrn_bwd(const float* x, wap_layout_t xl, const float* dy, wap_layout_t d
  * `work` holds `rows` floats (per-row losses, summed in row order). */
 int wap_xent_fwd_bwd(const float* logits, int64_t ldz, const float* labels, int64_t ldy, int rows, int cols,
                      float denominator, float* loss, float* dlogits, int64_t ldd, float* work, void* stream);
+/* Host-facing re-layout: unpack = 0 copies a dense [B,H,W,C] buffer into the
+ * layout `l` at `dst` (halo/lane padding untouched); unpack = 1 copies the
+ * layout at `dst` back into the dense buffer `dense` (used for graph outputs). */
+int wap_pack(const float* dense, wap_layout_t l, float* dst, int unpack, void* stream);
 /* SgdUpdate (interp.py:203-204): w_out = w - lr * g over n contiguous floats
  * (w_out may alias w: in-place update of the replicated variable). */
 int wap_sgd(const float* w, const float* g, float lr, float* w_out, int64_t n, void* stream);

@@ -118,8 +118,8 @@ _SIGNATURES: list[tuple[str, object, list]] = [
     ("wap_gemm_plan_create", _I, [C.POINTER(wap_gemm_desc_t), C.POINTER(_P)]),
     ("wap_gemm_plan_run", _I, [_P, _P]),
     ("wap_gemm_plan_destroy", None, [_P]),
-    ("wap_im2col", _I, [_P, wap_layout_t, _I, _I, _I, _I, _I, _P, _I64, _P]),
-    ("wap_col2im", _I, [_P, _I64, _I, _I, _I, _I, _I, _P, wap_layout_t, _P, wap_layout_t, _P]),
+    ("wap_im2col", _I, [_P, wap_layout_t, _I, _I, _I, _I, _I, _I, _P, _I64, _P]),
+    ("wap_col2im", _I, [_P, _I64, _I, _I, _I, _I, _I, _I, _P, wap_layout_t, _P, wap_layout_t, _P]),
     ("wap_elementwise", _I, [_I, _P, wap_layout_t, _P, wap_layout_t, _P, _P, wap_layout_t, _P]),
     ("wap_add_n", _I, [C.POINTER(_P), _I, wap_layout_t, _P, _P]),
     ("wap_bias_grad_work_floats", _I64, [wap_layout_t]),
@@ -130,6 +130,7 @@ _SIGNATURES: list[tuple[str, object, list]] = [
     ("wap_lrn_bwd", _I, [_P, wap_layout_t, _P, wap_layout_t, _I, _F, _F, _F, _P, wap_layout_t, _P,
                          wap_layout_t, _P]),
     ("wap_xent_fwd_bwd", _I, [_P, _I64, _P, _I64, _I, _I, _F, _P, _P, _I64, _P, _P]),
+    ("wap_pack", _I, [_P, wap_layout_t, _P, _I, _P]),
     ("wap_sgd", _I, [_P, _P, _F, _P, _I64, _P]),
     ("wap_wau_select", _I, [C.POINTER(wap_wau_layer_t), _I, _I64, _I, wap_wau_profile_t, _I, _P, _P,
                             _P, _P, _P, _P]),

@@ -127,11 +127,14 @@ int bias_chunks(const wap_layout_t& l) {
 // ---------------------------------------------------------------------------
 // im2col / col2im
 // ---------------------------------------------------------------------------
+// Rows of `col` enumerate the OUTPUT grid padded by P (halo rows are zero), so a
+// conv whose output must live on a padded grid gets GEMM rows that line up with it.
 __global__ void im2col_kernel(const float* __restrict__ x, wap_layout_t xl, int k, int s, int p, int Ho, int Wo,
-                              float* __restrict__ col, int64_t ldcol) {
+                              int P, float* __restrict__ col, int64_t ldcol) {
   const int C = xl.C;
   const int K = k * k * C;
-  const int64_t M = (int64_t)xl.B * Ho * Wo;
+  const int Hp = Ho + 2 * P, Wp = Wo + 2 * P;
+  const int64_t M = (int64_t)xl.B * Hp * Wp;
   const int64_t total = M * ldcol;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int kk = (int)(i % ldcol);
@@ -141,20 +144,22 @@ __global__ void im2col_kernel(const float* __restrict__ x, wap_layout_t xl, int 
       const int c = kk % C;
       const int t = kk / C;
       const int u = t / k, vv = t % k;
-      const int wo = (int)(m % Wo);
-      const int64_t r = m / Wo;
-      const int ho = (int)(r % Ho);
-      const int b = (int)(r / Ho);
+      const int wo = (int)(m % Wp) - P;
+      const int64_t r = m / Wp;
+      const int ho = (int)(r % Hp) - P;
+      const int b = (int)(r / Hp);
       const int hi = ho * s + u - p, wi = wo * s + vv - p;
-      if (hi >= 0 && hi < xl.H && wi >= 0 && wi < xl.W) v = __ldg(x + lidx(xl, b, hi, wi, c));
+      if (ho >= 0 && ho < Ho && wo >= 0 && wo < Wo && hi >= 0 && hi < xl.H && wi >= 0 && wi < xl.W)
+        v = __ldg(x + lidx(xl, b, hi, wi, c));
     }
     col[i] = v;
   }
 }
 
 __global__ void col2im_kernel(const float* __restrict__ dcol, int64_t ldcol, int k, int s, int p, int Ho, int Wo,
-                              float* __restrict__ dx, wap_layout_t dl, const float* __restrict__ mask,
+                              int P, float* __restrict__ dx, wap_layout_t dl, const float* __restrict__ mask,
                               wap_layout_t ml) {
+  const int Hp = Ho + 2 * P, Wp = Wo + 2 * P;
   const int C = dl.C;
   const int64_t total = (int64_t)dl.B * dl.H * dl.W * dl.ld;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -176,7 +181,7 @@ __global__ void col2im_kernel(const float* __restrict__ dcol, int64_t ldcol, int
           if (ws < 0 || ws % s) continue;
           const int wo = ws / s;
           if (wo >= Wo) continue;
-          acc += dcol[(((int64_t)b * Ho + ho) * Wo + wo) * ldcol + (u * k + v) * C + c];
+          acc += dcol[(((int64_t)b * Hp + ho + P) * Wp + wo + P) * ldcol + (u * k + v) * C + c];
         }
       }
       if (mask && !(mask[lidx(ml, b, h, w, c)] > 0.f)) acc = 0.f;
@@ -434,6 +439,22 @@ __global__ void xent_final_kernel(const float* __restrict__ row_loss, int rows, 
   }
 }
 
+// dense [B,H,W,C] (any C) <-> layout; dir 0 = pack dense->layout, 1 = unpack layout->dense
+__global__ void pack_kernel(const float* __restrict__ src, float* __restrict__ dst, wap_layout_t l, int dir) {
+  const int64_t total = (int64_t)l.B * l.H * l.W * l.C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % l.C);
+    int64_t q = i / l.C;
+    const int w = (int)(q % l.W);
+    q /= l.W;
+    const int h = (int)(q % l.H);
+    const int b = (int)(q / l.H);
+    const int64_t j = lidx(l, b, h, w, c);
+    if (dir == 0) dst[j] = src[i];
+    else dst[i] = src[j];
+  }
+}
+
 __global__ void sgd_kernel(const float* __restrict__ w, const float* __restrict__ g, float lr, float* __restrict__ o,
                            int64_t n) {
   const int64_t n4 = n / 4;
@@ -515,27 +536,29 @@ extern "C" int wap_bias_grad(const float* dy, wap_layout_t l, float* db, float* 
 }
 
 extern "C" int wap_im2col(const float* x, wap_layout_t xl, int k, int stride, int padding, int Ho, int Wo,
-                          float* col, int64_t ldcol, void* stream) {
+                          int out_pad, float* col, int64_t ldcol, void* stream) {
   int rc;
   if ((rc = check_layout(xl, "x"))) return rc;
-  WAP_CHECK_ARG(k >= 1 && stride >= 1 && padding >= 0 && Ho >= 1 && Wo >= 1, "im2col: bad geometry");
+  WAP_CHECK_ARG(k >= 1 && stride >= 1 && padding >= 0 && Ho >= 1 && Wo >= 1 && out_pad >= 0, "im2col: bad geometry");
   WAP_CHECK_ARG(ldcol >= (int64_t)k * k * xl.C, "im2col: ldcol too small");
-  const int64_t total = (int64_t)xl.B * Ho * Wo * ldcol;
-  im2col_kernel<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(x, xl, k, stride, padding, Ho, Wo, col, ldcol);
+  const int64_t total = (int64_t)xl.B * (Ho + 2 * out_pad) * (Wo + 2 * out_pad) * ldcol;
+  im2col_kernel<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(x, xl, k, stride, padding, Ho, Wo, out_pad, col,
+                                                                 ldcol);
   WAP_LAUNCH_CHECK();
   COUNT_LAUNCH();
   return WAP_OK;
 }
 
 extern "C" int wap_col2im(const float* dcol, int64_t ldcol, int k, int stride, int padding, int Ho, int Wo,
-                          float* dx, wap_layout_t dxl, const float* mask, wap_layout_t ml, void* stream) {
+                          int out_pad, float* dx, wap_layout_t dxl, const float* mask, wap_layout_t ml,
+                          void* stream) {
   int rc;
   if ((rc = check_layout(dxl, "dx"))) return rc;
   if (mask && (rc = check_layout(ml, "mask"))) return rc;
   WAP_CHECK_ARG(ldcol >= (int64_t)k * k * dxl.C, "col2im: ldcol too small");
   const int64_t total = (int64_t)dxl.B * dxl.H * dxl.W * dxl.ld;
-  col2im_kernel<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(dcol, ldcol, k, stride, padding, Ho, Wo, dx, dxl,
-                                                                 mask, ml);
+  col2im_kernel<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(dcol, ldcol, k, stride, padding, Ho, Wo, out_pad,
+                                                                 dx, dxl, mask, ml);
   WAP_LAUNCH_CHECK();
   COUNT_LAUNCH();
   return WAP_OK;
@@ -610,6 +633,17 @@ extern "C" int wap_xent_fwd_bwd(const float* logits, int64_t ldz, const float* l
   xent_final_kernel<<<1, 32, 0, STREAM(stream)>>>(work, rows, loss);
   WAP_LAUNCH_CHECK();
   g_wap_launches.fetch_add(2, std::memory_order_relaxed);
+  return WAP_OK;
+}
+
+extern "C" int wap_pack(const float* dense, wap_layout_t l, float* dst, int unpack, void* stream) {
+  WAP_CHECK_ARG(dense && dst, "pack: null pointer");
+  WAP_CHECK_ARG(l.B >= 1 && l.H >= 1 && l.W >= 1 && l.C >= 1 && l.ld >= l.C && l.pad >= 0, "pack: bad layout");
+  const int64_t total = (int64_t)l.B * l.H * l.W * l.C;
+  if (unpack) pack_kernel<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(dst, const_cast<float*>(dense), l, 1);
+  else pack_kernel<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(dense, dst, l, 0);
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
   return WAP_OK;
 }
 

@@ -1,0 +1,917 @@
+"""GPU runtime: lower a (per-device) WAP training graph to a static sequence of
+sm_100a kernel launches over preallocated HBM buffers.
+
+This is the B200 replacement of the reference's per-OpKind interpreter loop
+(interp.py:145-210). Instead of evaluating nodes one by one in fp64 numpy, a
+`Program`:
+
+1. chooses a strategy per Conv2D: `shifted` (stride-1 same conv with Ci % 32
+   == 0: a tcgen05 shifted GEMM over the padded-flat NHWC grid, no im2col
+   traffic) or `im2col` (first layers / strided / odd channel counts: one im2col
+   pass, then the same tcgen05 GEMM; the column buffer is reused by the weight
+   gradient);
+2. fuses what the reference keeps as separate nodes: Conv2D/MatMul + BiasAdd +
+   ReLU in the GEMM epilogue, GradReLU into the producer of its upstream
+   gradient (dgrad / FC-dX epilogue, MaxPool/LRN backward, col2im),
+   SoftmaxXentLoss + GradSoftmaxXent in one kernel;
+3. assigns every tensor a layout (NHWC with a zero halo of `pad` pixels and a
+   channel stride `ld` rounded to 4) by solving "same grid" constraints with a
+   union-find, so a conv's input, output, gradients and weight-gradient
+   operands share one padded-flat grid;
+4. allocates all buffers once (variables and their gradients in two flat
+   arenas with identical offsets, so SGD and the gradient allreduce are
+   contiguous bucket operations), pre-encodes every TMA descriptor, and records
+   the launch list; `run()` replays it on the current stream and `capture()`
+   turns it into a CUDA graph.
+
+Graph outputs keep the reference semantics exactly (loss = shard mean,
+updated variables), so `execute()` in interp.py is a drop-in for
+`wap.interp.execute`. There is no host fallback: without the native library
+every constructor raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .errors import EvalError
+from .ir import Graph, Node, OpKind, conv_geometry, infer_shapes, topo_order
+
+SHIFTED_MAX_TAPS = N.MAX_TAPS
+
+
+def _ceil4(x: int) -> int:
+    return (x + 3) // 4 * 4
+
+
+class _UF:
+    def __init__(self):
+        self.p: dict[str, str] = {}
+
+    def find(self, a: str) -> str:
+        self.p.setdefault(a, a)
+        while self.p[a] != a:
+            self.p[a] = self.p[self.p[a]]
+            a = self.p[a]
+        return a
+
+    def union(self, a: str, b: str) -> None:
+        ra, rb = self.find(a), self.find(b)
+        if ra != rb:
+            self.p[rb] = ra
+
+
+@dataclass
+class Tensor:
+    """A device buffer plus its layout. `dims` are the logical dims."""
+
+    dims: tuple[int, ...]
+    pad: int
+    ld: int
+    buf: object  # torch.Tensor (storage view)
+    kind: str    # 'nhwc' | 'mat' | 'vec' | 'kkio'
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+    def layout(self) -> N.wap_layout_t:
+        l = N.wap_layout_t()
+        if self.kind == "nhwc":
+            b, h, w, c = self.dims
+            l.B, l.H, l.W, l.C, l.pad = b, h, w, c, self.pad
+        elif self.kind == "mat":
+            l.B, l.H, l.W, l.C, l.pad = self.dims[0], 1, 1, self.dims[1], 0
+        elif self.kind == "kkio":
+            k, _, ci, co = self.dims
+            l.B, l.H, l.W, l.C, l.pad = k * k * ci, 1, 1, co, 0
+        else:  # vec
+            l.B, l.H, l.W, l.C, l.pad = 1, 1, 1, self.dims[0], 0
+        l.ld = self.ld
+        return l
+
+    @property
+    def rows(self) -> int:
+        """Rows of the 2D [rows, ld] view (padded grid rows for NHWC)."""
+        if self.kind == "nhwc":
+            b, h, w, _ = self.dims
+            return b * (h + 2 * self.pad) * (w + 2 * self.pad)
+        if self.kind == "mat":
+            return self.dims[0]
+        if self.kind == "kkio":
+            k, _, ci, _ = self.dims
+            return k * k * ci
+        return 1
+
+    def numel_storage(self) -> int:
+        return self.rows * self.ld
+
+
+def storage_kind(dims: tuple[int, ...], is_conv_weight: bool = False) -> str:
+    if is_conv_weight:
+        return "kkio"
+    return {4: "nhwc", 2: "mat", 1: "vec"}.get(len(dims), "bad")
+
+
+@dataclass
+class Step:
+    name: str
+    fn: object
+    args: tuple
+    what: str = ""
+    keep: list = field(default_factory=list)  # objects that must outlive the step (plans, ctypes arrays)
+
+    def __call__(self, stream: int) -> None:
+        rc = self.fn(*self.args, stream) if self.fn is not None else 0
+        if rc:
+            N.check(rc, f"{self.what or self.name}")
+
+
+class _GemmStep:
+    def __init__(self, name, call):
+        self.name = name
+        self.call = call
+
+    def __call__(self, stream: int) -> None:
+        N.check(N.lib().wap_gemm_plan_run(self.call._plan, stream), f"gemm {self.name}")
+
+
+class Program:
+    """A lowered training step for one device.
+
+    graph:        a training graph (single-device, a transformed multi-device
+                  graph evaluated in this one process, or a rank view whose
+                  AllReduceSum nodes have a single local input).
+    precision:    3 = 3xTF32 (fp32-accurate, default), 1 = TF32.
+    in_place:     SgdUpdate overwrites the variable buffers (training loop);
+                  otherwise updates go to fresh output buffers (execute()).
+    collective:   callable(list[(offset, numel)] , arena_tensor) performing the
+                  cross-rank SUM of gradient slices (None: single process).
+    """
+
+    def __init__(self, graph: Graph, precision: int = 3, device=None, in_place: bool = False,
+                 collective=None):
+        import torch
+
+        self.torch = torch
+        self.L = N.lib()
+        if not torch.cuda.is_available():
+            raise N.NativeUnavailable("CUDA device required: the WAP runtime has no host fallback")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.g = infer_shapes(graph)
+        self.order = topo_order(self.g)
+        self.users = self.g.consumers()
+        self.precision = precision
+        self.in_place = in_place
+        self.collective = collective
+        self.t: dict[str, Tensor] = {}
+        self.steps: list = []
+        self.update_steps: list = []
+        self.graph_exec = None
+        with torch.cuda.device(self.device):
+            self._analyze()
+            self._layouts()
+            self._allocate()
+            self._lower()
+
+    # ------------------------------------------------------------------ utils
+    def node(self, nid: str) -> Node:
+        return self.g.node(nid)
+
+    def dims(self, nid: str) -> tuple[int, ...]:
+        return self.g.node(nid).output_shape.dims
+
+    def kind(self, nid: str) -> OpKind:
+        return self.g.node(nid).kind
+
+    # --------------------------------------------------------------- analysis
+    def _conv_of_weight(self, w: str) -> str:
+        convs = [u for u in self.users[w] if self.kind(u) is OpKind.CONV2D and self.node(u).inputs[1] == w]
+        if len(convs) != 1:
+            raise EvalError(f"cannot associate weight {w!r} with a unique Conv2D")
+        return convs[0]
+
+    def _conv_of_wgrad(self, n: Node) -> str:
+        x, g = n.inputs
+        k = n.attr("kernel_size")
+        cands = [u for u in self.users[x] if self.kind(u) is OpKind.CONV2D and self.node(u).inputs[0] == x
+                 and self.node(u).device == n.device
+                 and self.dims(self.node(u).inputs[1])[0] == k and self.dims(u) == self.dims(g)
+                 and conv_geometry(self.node(u), k) == conv_geometry(n, k)]
+        if len(cands) != 1:
+            raise EvalError(f"cannot associate {n.id!r} with a unique Conv2D")
+        return cands[0]
+
+    def _analyze(self) -> None:
+        g = self.g
+        outputs = set(g.outputs)
+        self.strategy: dict[str, str] = {}
+        for nid in self.order:
+            n = self.node(nid)
+            if n.kind is OpKind.CONV2D:
+                k = self.dims(n.inputs[1])[0]
+                s, p = conv_geometry(n, k)
+                ci = self.dims(n.inputs[0])[3]
+                ok = s == 1 and p == k // 2 and k % 2 == 1 and ci % 32 == 0 and k * k <= SHIFTED_MAX_TAPS
+                self.strategy[nid] = "shifted" if ok else "im2col"
+        # forward epilogue fusion: producer -> (bias node | None, relu node | None)
+        self.fwd_fuse: dict[str, tuple[str | None, str | None]] = {}
+        self.virtual: set[str] = set()
+        self.mask_alias: dict[str, str] = {}
+        for nid in self.order:
+            n = self.node(nid)
+            if n.kind not in (OpKind.CONV2D, OpKind.MATMUL) or nid in outputs:
+                continue
+            us = self.users[nid]
+            if len(us) != 1 or self.kind(us[0]) is not OpKind.BIAS_ADD or self.node(us[0]).inputs[0] != nid:
+                continue
+            zb = us[0]
+            if self.kind(self.node(zb).inputs[1]) is not OpKind.VARIABLE:
+                continue
+            zu = self.users[zb]
+            relus = [u for u in zu if self.kind(u) is OpKind.RELU]
+            others = [u for u in zu if u not in relus]
+            if len(relus) == 1 and zb not in outputs and \
+                    all(self.kind(u) is OpKind.GRAD_RELU and self.node(u).inputs[0] == zb for u in others):
+                r = relus[0]
+                self.fwd_fuse[nid] = (zb, r)
+                self.virtual |= {nid, zb}
+                self.mask_alias[zb] = r
+            else:
+                self.fwd_fuse[nid] = (zb, None)
+                self.virtual.add(nid)
+        # a shifted conv's output lives on its input's padded grid; a conv that
+        # feeds a flattening MatMul needs compact rows instead -> im2col
+        flat_inputs = {self.node(u).inputs[0] for u in self.order
+                       if self.kind(u) in (OpKind.MATMUL, OpKind.GRAD_MATMUL_W) and self.node(u).attr("flatten_lhs")}
+        for nid, strat in self.strategy.items():
+            if strat == "shifted" and self.fused_out(nid) in flat_inputs:
+                self.strategy[nid] = "im2col"
+        # backward: GradReLU fused into the producer of its upstream gradient
+        self.bwd_mask: dict[str, str] = {}  # producer -> GradReLU node it writes for
+        fusable = (OpKind.GRAD_MATMUL_X, OpKind.GRAD_CONV2D_X, OpKind.GRAD_MAX_POOL, OpKind.GRAD_LRN)
+        for nid in self.order:
+            n = self.node(nid)
+            if n.kind is not OpKind.GRAD_RELU:
+                continue
+            prod = n.inputs[1]
+            if self.kind(prod) in fusable and self.users[prod] == [nid] and prod not in outputs:
+                self.bwd_mask[prod] = nid
+                self.virtual.add(prod)
+        # softmax cross-entropy pairs
+        self.xent: dict[tuple[str, str], dict[str, str]] = {}
+        for nid in self.order:
+            n = self.node(nid)
+            if n.kind in (OpKind.SOFTMAX_XENT_LOSS, OpKind.GRAD_SOFTMAX_XENT):
+                key = tuple(n.inputs)
+                self.xent.setdefault(key, {})["loss" if n.kind is OpKind.SOFTMAX_XENT_LOSS else "grad"] = nid
+        # MaxPool argmax owners: (input, window, stride) -> MaxPool node
+        self.pool_of: dict[tuple, str] = {}
+        for nid in self.order:
+            n = self.node(nid)
+            if n.kind is OpKind.MAX_POOL:
+                self.pool_of[(n.inputs[0], n.attr("window"), n.attr("stride"))] = nid
+
+    def mask_src(self, nid: str) -> str:
+        return self.mask_alias.get(nid, nid)
+
+    def fused_out(self, nid: str) -> str:
+        """The tensor a (possibly fused) Conv2D/MatMul actually writes."""
+        if nid in self.fwd_fuse:
+            zb, r = self.fwd_fuse[nid]
+            return r if r is not None else zb
+        return nid
+
+    # ---------------------------------------------------------------- layouts
+    def _layouts(self) -> None:
+        uf = _UF()
+        lb: dict[str, int] = {}
+        for nid in self.order:
+            uf.find(nid)
+
+        def need(t, p):
+            lb[t] = max(lb.get(t, 0), p)
+
+        for nid, (zb, r) in self.fwd_fuse.items():
+            uf.union(nid, zb)
+            if r is not None:
+                uf.union(nid, r)
+        for prod, gr in self.bwd_mask.items():
+            uf.union(prod, gr)
+        for nid in self.order:
+            n = self.node(nid)
+            if n.kind is OpKind.CONV2D:
+                out = self.fused_out(nid)
+                if self.strategy[nid] == "shifted":
+                    k = self.dims(n.inputs[1])[0]
+                    uf.union(n.inputs[0], out)
+                    need(n.inputs[0], k // 2)
+            elif n.kind is OpKind.GRAD_CONV2D_X:
+                conv = self._conv_of_weight(n.inputs[1])
+                uf.union(n.inputs[0], self.fused_out(conv))
+                if self.strategy[conv] == "shifted":
+                    uf.union(nid, self.node(conv).inputs[0])
+                    if nid in self.bwd_mask:
+                        uf.union(nid, self.mask_src(self.node(self.bwd_mask[nid]).inputs[0]))
+            elif n.kind is OpKind.GRAD_CONV2D_W:
+                conv = self._conv_of_wgrad(n)
+                uf.union(n.inputs[1], self.fused_out(conv))
+                if self.strategy[conv] == "shifted":
+                    uf.union(n.inputs[0], self.fused_out(conv))
+            elif n.kind is OpKind.GRAD_MATMUL_X and nid in self.bwd_mask:
+                uf.union(nid, self.mask_src(self.node(self.bwd_mask[nid]).inputs[0]))
+            elif n.kind is OpKind.SPLIT:
+                uf.union(nid, n.inputs[0])
+            elif n.kind in (OpKind.ADD_N, OpKind.ALL_REDUCE_SUM):
+                for i in n.inputs:
+                    uf.union(nid, i)
+            elif n.kind is OpKind.GRAD_RELU and nid not in self.bwd_mask.values():
+                pass  # elementwise kernel handles any pair of layouts
+        pad_of_class: dict[str, int] = {}
+        for t, p in lb.items():
+            r = uf.find(t)
+            pad_of_class[r] = max(pad_of_class.get(r, 0), p)
+        self.pad = {nid: (pad_of_class.get(uf.find(nid), 0) if len(self.dims(nid)) == 4 else 0)
+                    for nid in self.order}
+        # flatten MatMul inputs must be compact rows
+        for nid in self.order:
+            n = self.node(nid)
+            if n.kind in (OpKind.MATMUL, OpKind.GRAD_MATMUL_W) and n.attr("flatten_lhs"):
+                x = n.inputs[0]
+                d = self.dims(x)
+                if self.pad[x] or d[-1] % 4:
+                    raise EvalError(f"flatten of {x!r} needs an unpadded layout with C % 4 == 0, got pad "
+                                    f"{self.pad[x]} C {d[-1]}")
+
+    # ------------------------------------------------------------- allocation
+    def _new(self, dims, pad=0, kind=None, zero=True, arena=None) -> Tensor:
+        torch = self.torch
+        kind = kind or storage_kind(dims)
+        ld = _ceil4(dims[-1])
+        t = Tensor(tuple(dims), pad, ld, None, kind)
+        n = t.numel_storage()
+        if arena is not None:
+            t.buf = arena(n)
+        else:
+            alloc = torch.zeros if zero else torch.empty
+            t.buf = alloc(n, dtype=torch.float32, device=self.device)
+        return t
+
+    def _allocate(self) -> None:
+        torch = self.torch
+        g = self.g
+        # variables and their update gradients live in two arenas with equal offsets
+        self.var_ids = [nid for nid in self.order if self.kind(nid) is OpKind.VARIABLE]
+        conv_w = {self.node(u).inputs[1] for u in self.order if self.kind(u) is OpKind.CONV2D}
+        sizes = {}
+        for v in self.var_ids:
+            d = self.dims(v)
+            t = Tensor(d, 0, _ceil4(d[-1]), None, storage_kind(d, v in conv_w))
+            sizes[v] = _ceil4(t.numel_storage())
+        # gradient arena ordered by reverse topological position of the update
+        # (= the order backward produces gradients) so buckets are contiguous
+        self.updates = [nid for nid in self.order if self.kind(nid) is OpKind.SGD_UPDATE]
+        order_pos = {nid: i for i, nid in enumerate(self.order)}
+
+        def grad_ready(u):
+            return order_pos[self.node(u).inputs[1]]
+
+        upd_sorted = sorted(self.updates, key=grad_ready, reverse=True)
+        arena_vars = [self.node(u).inputs[0] for u in upd_sorted]
+        arena_vars += [v for v in self.var_ids if v not in arena_vars]
+        self.arena_off: dict[str, int] = {}
+        off = 0
+        for v in arena_vars:
+            self.arena_off[v] = off
+            off += sizes[v]
+        self.arena_numel = max(off, 4)
+        self.var_arena = torch.zeros(self.arena_numel, dtype=torch.float32, device=self.device)
+        self.grad_arena = torch.zeros(self.arena_numel, dtype=torch.float32, device=self.device)
+        for v in self.var_ids:
+            d = self.dims(v)
+            o = self.arena_off[v]
+            self.t[v] = Tensor(d, 0, _ceil4(d[-1]), self.var_arena[o:o + sizes[v]], storage_kind(d, v in conv_w))
+        # the gradient each update consumes is written straight into the grad arena
+        self.grad_slot: dict[str, str] = {}
+        for u in self.updates:
+            v, gsrc = self.node(u).inputs
+            o = self.arena_off[v]
+            d = self.dims(v)
+            if gsrc in self.t or self.kind(gsrc) in (OpKind.VARIABLE, OpKind.INPUT):
+                continue
+            target = gsrc
+            gn = self.node(gsrc)
+            if gn.kind is OpKind.ALL_REDUCE_SUM and len(gn.inputs) == 1:
+                target = gn.inputs[0]  # rank view: the local gradient IS the allreduce buffer
+            slot = Tensor(d, 0, _ceil4(d[-1]), self.grad_arena[o:o + sizes[v]], storage_kind(d, v in conv_w))
+            self.t[target] = slot
+            self.t[gsrc] = slot
+            self.grad_slot[target] = v
+        # activations / gradients
+        for nid in self.order:
+            n = self.node(nid)
+            if nid in self.t or nid in self.virtual:
+                continue
+            if n.kind is OpKind.SPLIT:
+                continue  # views, created during lowering
+            if n.kind is OpKind.SGD_UPDATE:
+                v = n.inputs[0]
+                if self.in_place:
+                    self.t[nid] = self.t[v]
+                else:
+                    d = self.dims(nid)
+                    self.t[nid] = self._new(d, 0, kind=self.t[v].kind)
+                continue
+            d = self.dims(nid)
+            if n.kind in (OpKind.GRAD_CONV2D_W,):
+                self.t[nid] = self._new(d, 0, kind="kkio")
+                continue
+            if n.kind is OpKind.ALL_REDUCE_SUM and len(n.inputs) == 1:
+                raise EvalError(f"rank-local AllReduceSum {nid!r} must feed an SgdUpdate")
+            self.t[nid] = self._new(d, self.pad.get(nid, 0))
+        # aliases for fused/virtual producers
+        for nid, (zb, r) in self.fwd_fuse.items():
+            if r is not None:
+                self.t[zb] = self.t[r]  # mask source: relu(x) > 0  <=>  x > 0
+
+    # ---------------------------------------------------------------- lowering
+    def _emit(self, name, fn, args, what="", keep=None):
+        self.steps.append(Step(name, fn, tuple(args), what, keep or []))
+
+    def _gemm(self, name, M, Nn, K, a, b, out: Tensor, bias=None, relu=False, mask: Tensor | None = None,
+              halo=(0, 0, 0), splits=0, to_updates=False):
+        from .kernels import GemmCall
+
+        d = N.wap_gemm_desc_t()
+        d.M, d.N, d.K = M, Nn, K
+        d.a, d.b = a, b
+        d.c = out.ptr
+        d.ldc = out.ld
+        d.bias = bias.ptr if bias is not None else None
+        d.relu = 1 if relu else 0
+        d.mask = mask.ptr if mask is not None else None
+        d.ldm = mask.ld if mask is not None else 0
+        d.halo_pad, d.halo_h, d.halo_w = halo
+        d.precision = self.precision
+        d.splits = splits
+        call = GemmCall(d, device=self.device)
+        step = _GemmStep(name, call)
+        (self.update_steps if to_updates else self.steps).append(step)
+        return call
+
+    def _operand(self, t: Tensor, mn_major: bool, inner: int | None = None, tap_period=0, offsets=(0,)):
+        return N.operand(t.ptr, inner=inner if inner is not None else t.dims[-1], outer=t.rows, ld=t.ld,
+                         mn_major=mn_major, tap_period=tap_period, offsets=offsets)
+
+    def _lower(self) -> None:
+        L = self.L
+        for nid in self.order:
+            n = self.node(nid)
+            k = n.kind
+            if k in (OpKind.INPUT, OpKind.VARIABLE):
+                continue
+            if k is OpKind.CONV2D:
+                self._lower_conv(n)
+            elif k is OpKind.MATMUL:
+                self._lower_matmul(n)
+            elif k is OpKind.BIAS_ADD:
+                if self.node(n.inputs[0]).id in self.fwd_fuse:
+                    continue  # fused into the GEMM epilogue
+                self._elementwise(0, n.inputs[0], None, n.inputs[1], nid)
+            elif k is OpKind.RELU:
+                if n.inputs[0] in self.mask_alias and self.mask_alias[n.inputs[0]] == nid:
+                    continue  # fused
+                self._elementwise(1, n.inputs[0], None, None, nid)
+            elif k is OpKind.GRAD_RELU:
+                if nid in self.bwd_mask.values():
+                    continue  # written by the fused producer
+                self._elementwise(3, n.inputs[1], self.mask_src(n.inputs[0]), None, nid)
+            elif k in (OpKind.SOFTMAX_XENT_LOSS, OpKind.GRAD_SOFTMAX_XENT):
+                self._lower_xent(n)
+            elif k is OpKind.GRAD_BIAS:
+                self._lower_bias_grad(n)
+            elif k is OpKind.GRAD_MATMUL_W:
+                self._lower_matmul_w(n)
+            elif k is OpKind.GRAD_MATMUL_X:
+                self._lower_matmul_x(n)
+            elif k is OpKind.GRAD_CONV2D_W:
+                self._lower_conv_w(n)
+            elif k is OpKind.GRAD_CONV2D_X:
+                self._lower_conv_x(n)
+            elif k is OpKind.MAX_POOL:
+                self._lower_pool(n)
+            elif k is OpKind.GRAD_MAX_POOL:
+                self._lower_pool_grad(n)
+            elif k is OpKind.LRN:
+                self._lower_lrn(n)
+            elif k is OpKind.GRAD_LRN:
+                self._lower_lrn_grad(n)
+            elif k in (OpKind.ADD_N,):
+                self._lower_add_n(n)
+            elif k is OpKind.ALL_REDUCE_SUM:
+                self._lower_allreduce(n)
+            elif k is OpKind.SPLIT:
+                pass  # resolved by consumers (see _in)
+            elif k is OpKind.CONCAT:
+                self._lower_concat(n)
+            elif k is OpKind.SGD_UPDATE:
+                self._lower_sgd(n)
+            else:
+                raise EvalError(f"no GPU rule for kind {k.value}")
+        self.steps.extend(self.update_steps)
+        self.update_steps = []
+
+    # -- tensor access ---------------------------------------------------------
+    def _in(self, consumer: Node, nid: str) -> Tensor:
+        """Materialized input tensor; Split parts become row views."""
+        n = self.node(nid)
+        if n.kind is OpKind.SPLIT:
+            src = self._in(n, n.inputs[0])
+            parts = n.attr("parts")
+            if n.attr("axis") != 0:
+                raise EvalError("Split is supported along the batch axis (0) only")
+            dev = consumer.device
+            if dev is None or not 0 <= dev < parts:
+                raise EvalError(f"node {consumer.id!r} consumes split {nid!r} but has no part device")
+            per = src.numel_storage() // parts
+            dims = (src.dims[0] // parts,) + tuple(src.dims[1:])
+            kind = src.kind
+            return Tensor(dims, src.pad, src.ld, src.buf[dev * per:(dev + 1) * per], kind)
+        if nid not in self.t:
+            raise EvalError(f"tensor {nid!r} was not materialized")
+        return self.t[nid]
+
+    def _out(self, nid: str) -> Tensor:
+        return self.t[nid]
+
+    # -- forward -------------------------------------------------------------
+    def _lower_conv(self, n: Node) -> None:
+        x = self._in(n, n.inputs[0])
+        w = self._in(n, n.inputs[1])
+        kk, _, ci, co = w.dims
+        s, p = conv_geometry(n, kk)
+        zb, r = self.fwd_fuse.get(n.id, (None, None))
+        out_id = self.fused_out(n.id)
+        y = self._out(out_id)
+        bias = self._in(self.node(zb), self.node(zb).inputs[1]) if zb is not None else None
+        relu = r is not None
+        b, ho, wo, _ = self.dims(n.id)
+        if self.strategy[n.id] == "shifted":
+            P = x.pad
+            assert y.pad == P, (n.id, y.pad, P)
+            wp = x.dims[2] + 2 * P
+            shifts = [(u - p) * wp + (v - p) for u in range(kk) for v in range(kk)]
+            a = self._operand(x, False, inner=ci, tap_period=ci, offsets=tuple(shifts))
+            bo = N.operand(w.ptr, inner=co, outer=kk * kk * ci, ld=w.ld, mn_major=True)
+            self._gemm(n.id, x.rows, co, kk * kk * ci, a, bo, y, bias=bias, relu=relu, halo=(P, ho, wo))
+        else:
+            P = y.pad
+            K = kk * kk * ci
+            ldcol = _ceil4(K)
+            rows = b * (ho + 2 * P) * (wo + 2 * P)
+            col = self.torch.empty(rows * ldcol, dtype=self.torch.float32, device=self.device)
+            self.t[f"{n.id}::col"] = Tensor((rows, K), 0, ldcol, col, "mat")
+            self._emit(n.id + "/im2col", self.L.wap_im2col,
+                       (x.ptr, x.layout(), kk, s, p, ho, wo, P, col.data_ptr(), ldcol), "im2col")
+            ct = self.t[f"{n.id}::col"]
+            a = self._operand(ct, False, inner=K)
+            bo = N.operand(w.ptr, inner=co, outer=K, ld=w.ld, mn_major=True)
+            self._gemm(n.id, rows, co, K, a, bo, y, bias=bias, relu=relu, halo=(P, ho, wo) if P else (0, 0, 0))
+
+    def _lower_matmul(self, n: Node) -> None:
+        x = self._in(n, n.inputs[0])
+        w = self._in(n, n.inputs[1])
+        i, o = w.dims
+        zb, r = self.fwd_fuse.get(n.id, (None, None))
+        y = self._out(self.fused_out(n.id))
+        bias = self._in(self.node(zb), self.node(zb).inputs[1]) if zb is not None else None
+        rows = x.dims[0]
+        ld = x.ld if x.kind == "mat" else int(np.prod(x.dims[1:]))
+        a = N.operand(x.ptr, inner=i, outer=rows, ld=ld, mn_major=False)
+        bo = N.operand(w.ptr, inner=o, outer=i, ld=w.ld, mn_major=True)
+        self._gemm(n.id, rows, o, i, a, bo, y, bias=bias, relu=r is not None)
+
+    def _elementwise(self, op, x_id, aux_id, bias_id, out_id) -> None:
+        node = self.node(out_id)
+        x = self._in(node, x_id)
+        aux = self._in(node, aux_id) if aux_id is not None else None
+        bias = self._in(node, bias_id) if bias_id is not None else None
+        y = self._out(out_id)
+        xl, yl = self._as_compat(x, y)
+        al = self._as_compat(aux, y)[0] if aux is not None else N.wap_layout_t()
+        self._emit(out_id, self.L.wap_elementwise,
+                   (op, x.ptr, xl, aux.ptr if aux is not None else None, al,
+                    bias.ptr if bias is not None else None, y.ptr, yl), f"elementwise[{op}] {out_id}")
+
+    @staticmethod
+    def _as_compat(a: Tensor, b: Tensor):
+        """Layouts of a and b viewed with the same logical dims (flatten-aware)."""
+        la, lb = a.layout(), b.layout()
+        if (la.B, la.H, la.W, la.C) != (lb.B, lb.H, lb.W, lb.C):
+            if a.kind == "mat" and b.kind == "nhwc" and b.pad == 0 and b.ld == b.dims[-1]:
+                lb2 = N.wap_layout_t(la.B, la.H, la.W, la.C, 0, la.ld)
+                lb2.ld = int(np.prod(b.dims[1:]))
+                return la, lb2
+            if b.kind == "mat" and a.kind == "nhwc" and a.pad == 0 and a.ld == a.dims[-1]:
+                la2 = N.wap_layout_t(lb.B, lb.H, lb.W, lb.C, 0, int(np.prod(a.dims[1:])))
+                return la2, lb
+            raise EvalError(f"incompatible layouts {a.dims} vs {b.dims}")
+        return la, lb
+
+    def _lower_xent(self, n: Node) -> None:
+        key = tuple(n.inputs)
+        pair = self.xent[key]
+        first = pair.get("loss") or pair.get("grad")
+        if pair.get("loss") and pair.get("grad"):
+            # emit once, at the first of the two in topological order
+            pos = {x: i for i, x in enumerate(self.order)}
+            first = min(pair.values(), key=lambda x: pos[x])
+        if n.id != first:
+            return
+        z = self._in(n, n.inputs[0])
+        y = self._in(n, n.inputs[1])
+        rows, cols = z.dims
+        loss = self.t[pair["loss"]] if "loss" in pair else self._new((1,))
+        if "grad" in pair:
+            dz = self.t[pair["grad"]]
+            denom = self.node(pair["grad"]).attr("denominator", rows)
+        else:
+            dz = self._new((rows, cols))
+            denom = rows
+        work = self.torch.empty(rows, dtype=self.torch.float32, device=self.device)
+        self._emit(n.id + "/xent", self.L.wap_xent_fwd_bwd,
+                   (z.ptr, z.ld, y.ptr, y.ld, rows, cols, C.c_float(float(denom)), loss.ptr, dz.ptr, dz.ld,
+                    work.data_ptr()), "softmax-xent", keep=[work, loss, dz])
+
+    def _lower_bias_grad(self, n: Node) -> None:
+        dy = self._in(n, n.inputs[0])
+        db = self._out(n.id)
+        lay = dy.layout()
+        wf = self.L.wap_bias_grad_work_floats(lay)
+        work = self.torch.empty(max(wf, 1), dtype=self.torch.float32, device=self.device)
+        self._emit(n.id, self.L.wap_bias_grad, (dy.ptr, lay, db.ptr, work.data_ptr()), "GradBias", keep=[work])
+
+    # -- backward GEMMs ------------------------------------------------------
+    def _lower_matmul_w(self, n: Node) -> None:
+        x = self._in(n, n.inputs[0])
+        dy = self._in(n, n.inputs[1])
+        dw = self._out(n.id)
+        i, o = self.dims(n.id)
+        rows = x.dims[0]
+        ldx = x.ld if x.kind == "mat" else int(np.prod(x.dims[1:]))
+        a = N.operand(x.ptr, inner=i, outer=rows, ld=ldx, mn_major=True)
+        bo = N.operand(dy.ptr, inner=o, outer=rows, ld=dy.ld, mn_major=True)
+        self._gemm(n.id, i, o, rows, a, bo, dw)
+
+    def _lower_matmul_x(self, n: Node) -> None:
+        dy = self._in(n, n.inputs[0])
+        w = self._in(n, n.inputs[1])
+        i, o = w.dims
+        gr = self.bwd_mask.get(n.id)
+        out = self._out(gr if gr else n.id)
+        mask = self._in(self.node(gr), self.mask_src(self.node(gr).inputs[0])) if gr else None
+        rows = dy.dims[0]
+        a = N.operand(dy.ptr, inner=o, outer=rows, ld=dy.ld, mn_major=False)
+        bo = N.operand(w.ptr, inner=o, outer=i, ld=w.ld, mn_major=False)
+        flat_out = out if out.kind == "mat" else Tensor((rows, i), 0, int(np.prod(out.dims[1:])), out.buf, "mat")
+        flat_mask = None
+        if mask is not None:
+            flat_mask = mask if mask.kind == "mat" else Tensor((rows, i), 0, int(np.prod(mask.dims[1:])), mask.buf,
+                                                               "mat")
+        self._gemm(n.id, rows, i, o, a, bo, flat_out, mask=flat_mask)
+
+    def _lower_conv_x(self, n: Node) -> None:
+        dy = self._in(n, n.inputs[0])
+        w = self._in(n, n.inputs[1])
+        conv = self._conv_of_weight(n.inputs[1])
+        cn = self.node(conv)
+        kk, _, ci, co = w.dims
+        s, p = conv_geometry(cn, kk)
+        gr = self.bwd_mask.get(n.id)
+        out = self._out(gr if gr else n.id)
+        mask = self._in(self.node(gr), self.mask_src(self.node(gr).inputs[0])) if gr else None
+        b, ho, wo, _ = self.dims(conv)
+        if self.strategy[conv] == "shifted":
+            P = dy.pad
+            assert out.pad == P and (mask is None or (mask.pad == P and mask.ld == out.ld))
+            wp = out.dims[2] + 2 * P
+            shifts = [(u - p) * wp + (v - p) for u in range(kk) for v in range(kk)]
+            a = self._operand(dy, False, inner=co, tap_period=co, offsets=tuple(-s_ for s_ in shifts))
+            bo = N.operand(w.ptr, inner=co, outer=kk * kk * ci, ld=w.ld, mn_major=False, tap_period=co,
+                           offsets=tuple(t * ci for t in range(kk * kk)))
+            self._gemm(n.id, dy.rows, ci, kk * kk * co, a, bo, out, mask=mask, halo=(P, out.dims[1], out.dims[2]))
+        else:
+            P = dy.pad
+            K = kk * kk * ci
+            ldcol = _ceil4(K)
+            rows = dy.rows
+            dcol = self.torch.empty(rows * ldcol, dtype=self.torch.float32, device=self.device)
+            dct = Tensor((rows, K), 0, ldcol, dcol, "mat")
+            a = self._operand(dy, False, inner=co)
+            bo = N.operand(w.ptr, inner=co, outer=K, ld=w.ld, mn_major=False)
+            self._gemm(n.id + "/dcol", rows, K, co, a, bo, dct)
+            ml = mask.layout() if mask is not None else N.wap_layout_t()
+            self._emit(n.id + "/col2im", self.L.wap_col2im,
+                       (dcol.data_ptr(), ldcol, kk, s, p, ho, wo, P, out.ptr, out.layout(),
+                        mask.ptr if mask is not None else None, ml), "col2im", keep=[dcol])
+
+    def _lower_conv_w(self, n: Node) -> None:
+        x = self._in(n, n.inputs[0])
+        dy = self._in(n, n.inputs[1])
+        dw = self._out(n.id)
+        conv = self._conv_of_wgrad(n)
+        kk, _, ci, co = self.dims(n.id)
+        if self.strategy[conv] == "shifted":
+            P = x.pad
+            assert dy.pad == P
+            p = kk // 2
+            wp = x.dims[2] + 2 * P
+            shifts = [(u - p) * wp + (v - p) for u in range(kk) for v in range(kk)]
+            a = N.operand(x.ptr, inner=ci, outer=x.rows, ld=x.ld, mn_major=True, tap_period=ci,
+                          offsets=tuple(shifts))
+            bo = N.operand(dy.ptr, inner=co, outer=dy.rows, ld=dy.ld, mn_major=True)
+            self._gemm(n.id, kk * kk * ci, co, x.rows, a, bo, dw)
+        else:
+            col = self.t[f"{conv}::col"]
+            K = kk * kk * ci
+            assert col.rows == dy.rows, (n.id, col.rows, dy.rows)
+            a = N.operand(col.ptr, inner=K, outer=col.rows, ld=col.ld, mn_major=True)
+            bo = N.operand(dy.ptr, inner=co, outer=dy.rows, ld=dy.ld, mn_major=True)
+            self._gemm(n.id, K, co, col.rows, a, bo, dw)
+
+    # -- pooling / LRN -------------------------------------------------------
+    def _lower_pool(self, n: Node) -> None:
+        x = self._in(n, n.inputs[0])
+        y = self._out(n.id)
+        if x.ld != y.ld:
+            raise EvalError("MaxPool needs equal channel strides")
+        arg = self.torch.zeros(y.numel_storage(), dtype=self.torch.uint8, device=self.device)
+        self.t[f"{n.id}::argmax"] = Tensor(y.dims, y.pad, y.ld, arg, "nhwc")
+        self._emit(n.id, self.L.wap_maxpool_fwd,
+                   (x.ptr, x.layout(), n.attr("window"), n.attr("stride"), y.ptr, y.layout(), arg.data_ptr()),
+                   "MaxPool", keep=[arg])
+
+    def _lower_pool_grad(self, n: Node) -> None:
+        x_id, dy_id = n.inputs
+        pool = self.pool_of.get((x_id, n.attr("window"), n.attr("stride")))
+        if pool is None:
+            raise EvalError(f"{n.id!r}: no matching MaxPool forward for its argmax")
+        arg = self.t[f"{pool}::argmax"]
+        dy = self._in(n, dy_id)
+        gr = self.bwd_mask.get(n.id)
+        out = self._out(gr if gr else n.id)
+        mask = self._in(self.node(gr), self.mask_src(self.node(gr).inputs[0])) if gr else None
+        ml = mask.layout() if mask is not None else N.wap_layout_t()
+        if dy.pad != arg.pad:
+            raise EvalError("MaxPool gradient must share the pooled output layout")
+        self._emit(n.id, self.L.wap_maxpool_bwd,
+                   (arg.ptr, dy.ptr, dy.layout(), n.attr("window"), n.attr("stride"), out.ptr, out.layout(),
+                    mask.ptr if mask is not None else None, ml), "GradMaxPool")
+
+    def _lower_lrn(self, n: Node) -> None:
+        x = self._in(n, n.inputs[0])
+        y = self._out(n.id)
+        a = n.attrs
+        self._emit(n.id, self.L.wap_lrn_fwd,
+                   (x.ptr, x.layout(), a["size"], C.c_float(a["alpha"]), C.c_float(a["beta"]), C.c_float(a["bias"]),
+                    y.ptr, y.layout()), "LRN")
+
+    def _lower_lrn_grad(self, n: Node) -> None:
+        x = self._in(n, n.inputs[0])
+        dy = self._in(n, n.inputs[1])
+        gr = self.bwd_mask.get(n.id)
+        out = self._out(gr if gr else n.id)
+        mask = self._in(self.node(gr), self.mask_src(self.node(gr).inputs[0])) if gr else None
+        ml = mask.layout() if mask is not None else N.wap_layout_t()
+        a = n.attrs
+        self._emit(n.id, self.L.wap_lrn_bwd,
+                   (x.ptr, x.layout(), dy.ptr, dy.layout(), a["size"], C.c_float(a["alpha"]), C.c_float(a["beta"]),
+                    C.c_float(a["bias"]), out.ptr, out.layout(), mask.ptr if mask is not None else None, ml),
+                   "GradLRN")
+
+    # -- aggregation / update ------------------------------------------------
+    def _lower_add_n(self, n: Node) -> None:
+        ins = [self._in(n, i) for i in n.inputs]
+        out = self._out(n.id)
+        for t in ins:
+            if t.numel_storage() != out.numel_storage() or t.ld != out.ld or t.pad != out.pad:
+                raise EvalError(f"{n.id!r}: AddN operands must share one layout")
+        for lo in range(0, len(ins), 16):
+            chunk = ins[lo:lo + 16]
+            srcs = ([out] if lo else []) + chunk
+            srcs = srcs[:16]
+            arr = (C.c_void_p * len(srcs))(*[t.ptr for t in srcs])
+            self._emit(f"{n.id}#{lo}", self.L.wap_add_n, (arr, len(srcs), out.layout(), out.ptr), "AddN",
+                       keep=[arr])
+
+    def _lower_allreduce(self, n: Node) -> None:
+        if len(n.inputs) >= 2:  # all replicas in this process: left fold (interp.py:181-182)
+            self._lower_add_n(n)
+            return
+        # rank-local view: the sum crosses processes
+        src = self._in(n, n.inputs[0])
+        if self.collective is not None:
+            self.steps.append(_CollectiveStep(n.id, self.collective, src))
+
+    def _lower_concat(self, n: Node) -> None:
+        out = self._out(n.id)
+        if n.attr("axis") != 0:
+            raise EvalError("Concat is supported along the batch axis (0) only")
+        per = out.numel_storage() // len(n.inputs)
+        for k, i in enumerate(n.inputs):
+            src = self._in(n, i)
+            dst = Tensor(src.dims, out.pad, out.ld, out.buf[k * per:(k + 1) * per], out.kind)
+            xl, yl = self._as_compat(src, dst)
+            self._emit(f"{n.id}#{k}", self.L.wap_elementwise, (4, src.ptr, xl, None, N.wap_layout_t(), None,
+                                                                dst.ptr, yl), "Concat copy")
+
+    def _lower_sgd(self, n: Node) -> None:
+        v = self._in(n, n.inputs[0])
+        gsrc = self._in(n, n.inputs[1])
+        out = self._out(n.id)
+        lr = float(n.attr("learning_rate"))
+        if gsrc.numel_storage() != v.numel_storage():
+            raise EvalError(f"{n.id!r}: gradient layout does not match the variable")
+        self.update_steps.append(Step(n.id, self.L.wap_sgd,
+                                      (v.ptr, gsrc.ptr, C.c_float(lr), out.ptr, v.numel_storage()), "SgdUpdate"))
+
+    # ------------------------------------------------------------- execution
+    def run(self, stream=None) -> None:
+        s = N.stream_ptr(stream)
+        if self.graph_exec is not None:
+            self.graph_exec.replay()
+            return
+        for st in self.steps:
+            st(s)
+
+    def capture(self) -> None:
+        """Record the whole step as one CUDA graph (replayed by run())."""
+        torch = self.torch
+        if any(isinstance(s, _CollectiveStep) for s in self.steps):
+            raise EvalError("steps with cross-process collectives are not captured")
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            for st in self.steps:  # warm-up on the capture stream
+                st(N.stream_ptr(side))
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            for st in self.steps:
+                st(N.stream_ptr(side))
+        self.graph_exec = g
+
+    # ----------------------------------------------------------- host binding
+    def input_ids(self) -> list[str]:
+        return [nid for nid in self.order if self.kind(nid) is OpKind.INPUT]
+
+    def _upload(self, t: Tensor, value, stream=None) -> None:
+        torch = self.torch
+        src = value if isinstance(value, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(value))
+        src = src.to(dtype=torch.float32)
+        dev_src = src.to(self.device, non_blocking=True).contiguous()
+        dims = t.dims
+        lay = t.layout()
+        if t.kind == "nhwc" and tuple(dev_src.shape) != dims:
+            raise EvalError(f"binding has shape {tuple(dev_src.shape)}, expected {dims}")
+        N.check(self.L.wap_pack(dev_src.data_ptr(), lay, t.ptr, 0, N.stream_ptr(stream)), "pack")
+        self._keep_alive = dev_src
+
+    def bind(self, values: dict, stream=None) -> None:
+        """Copy host/torch arrays into Input (and optionally Variable) buffers."""
+        for k, v in values.items():
+            if k not in self.t or self.kind(k) not in (OpKind.INPUT, OpKind.VARIABLE):
+                continue
+            self._upload(self.t[k], v, stream)
+        self.torch.cuda.current_stream(self.device).synchronize()
+
+    def fetch(self, nid: str) -> np.ndarray:
+        torch = self.torch
+        t = self.t[nid]
+        dims = t.dims
+        dense = torch.empty(int(np.prod(dims)), dtype=torch.float32, device=self.device)
+        N.check(self.L.wap_pack(dense.data_ptr(), t.layout(), t.ptr, 1, N.stream_ptr()), "unpack")
+        return dense.cpu().numpy().reshape(dims)
+
+    def outputs(self) -> dict[str, np.ndarray]:
+        return {o: self.fetch(o) for o in self.g.outputs}
+
+    def launches_per_step(self) -> int:
+        before = N.launch_count()
+        self.run()
+        self.torch.cuda.synchronize()
+        return N.launch_count() - before
+
+
+class _CollectiveStep:
+    def __init__(self, name, fn, t: Tensor):
+        self.name = name
+        self.fn = fn
+        self.t = t
+
+    def __call__(self, stream: int) -> None:
+        self.fn(self.t.buf)
