@@ -209,10 +209,13 @@ def _topo(graph) -> list[str]:
     return order
 
 
-def execute(graph, inputs: dict[str, np.ndarray], seed: int = 0, keep: set[str] | None = None) -> dict[str, np.ndarray]:
+def execute(graph, inputs: dict[str, np.ndarray], seed: int = 0, keep: set[str] | None = None,
+            hooks: dict | None = None) -> dict[str, np.ndarray]:
     """Evaluate every node in topological order (ties by id); returns the graph
     outputs (plus any ids in `keep`). Works on the reference's Graph objects or
-    this package's (duck-typed: id, kind.value, inputs, attrs, device)."""
+    this package's (duck-typed: id, kind.value, inputs, attrs, device).
+    `hooks` maps a kind name to fn(node, input_values) overriding its rule
+    (tests use it to put a real gloo allreduce behind a rank-local AllReduceSum)."""
     vals: dict[str, object] = {}
     nodes = {n.id: n for n in graph}
 
@@ -238,6 +241,9 @@ def execute(graph, inputs: dict[str, np.ndarray], seed: int = 0, keep: set[str] 
                 vals[nid] = INIT_SCALE * rng(seed, "var", _base(nid)).standard_normal(tuple(a["shape"]))
             continue
         ins = [fetch(n, i) for i in n.inputs]
+        if hooks and kind in hooks:
+            vals[nid] = hooks[kind](n, ins)
+            continue
         if kind == "MatMul":
             x = ins[0].reshape(ins[0].shape[0], -1) if a.get("flatten_lhs") else ins[0]
             out = x @ ins[1]

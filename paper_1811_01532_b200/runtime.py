@@ -460,6 +460,12 @@ class Program:
         d.splits = splits
         call = GemmCall(d, device=self.device)
         step = _GemmStep(name, call)
+        from .workloads import node_flops
+
+        nid = name[:-5] if name.endswith("/dcol") else name
+        # algorithmic FLOPs by WAP's counting rule (workloads.py:84-117): no halo rows, no padding lanes
+        step.alg_flops = node_flops(self.g, nid) if nid in self.g.nodes else 2 * M * Nn * K
+        step.shape = (M, Nn, K)
         (self.update_steps if to_updates else self.steps).append(step)
         return call
 
@@ -888,6 +894,34 @@ class Program:
                 continue
             self._upload(self.t[k], v, stream)
         self.torch.cuda.current_stream(self.device).synchronize()
+
+    def bind_async(self, values: dict, stream=None) -> None:
+        """Stream-ordered binding for the training loop: pinned host (or device)
+        tensors -> preallocated dense staging -> layout pack; no synchronisation."""
+        torch = self.torch
+        if not hasattr(self, "_staging"):
+            self._staging = {}
+        s = N.stream_ptr(stream)
+        for k, v in values.items():
+            t = self.t[k]
+            n = int(np.prod(t.dims))
+            dense_ok = (t.pad == 0 and t.ld == t.dims[-1])
+            if isinstance(v, np.ndarray):
+                v = torch.from_numpy(v)
+            if v.dtype != torch.float32:
+                raise EvalError(f"binding {k!r} must be float32 for the async path")
+            if dense_ok:
+                t.buf[:n].copy_(v.reshape(-1), non_blocking=True)
+                continue
+            st = self._staging.get(k)
+            if st is None:
+                st = self._staging[k] = torch.empty(n, dtype=torch.float32, device=self.device)
+            if v.device.type == "cuda":
+                src = v.reshape(-1)
+            else:
+                st.copy_(v.reshape(-1), non_blocking=True)
+                src = st
+            N.check(self.L.wap_pack(src.data_ptr(), t.layout(), t.ptr, 0, s), "pack")
 
     def fetch(self, nid: str) -> np.ndarray:
         torch = self.torch
