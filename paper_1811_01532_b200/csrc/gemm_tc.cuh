@@ -1,0 +1,485 @@
+// tcgen05 (5th-gen tensor core) TF32 / 3xTF32 shifted-GEMM kernel for sm_100a.
+//
+// One template covers every dense contraction on the WAP hot path:
+//   MatMul        Y  = X W            A K-major,  B MN-major   (interp.py:162-163)
+//   GradMatMulX   dX = dY W^T         A K-major,  B K-major    (interp.py:185-189)
+//   GradMatMulW   dW = X^T dY         A MN-major, B MN-major   (interp.py:183-184)
+//   Conv2D        shifted GEMM over the padded-flat NHWC grid: A rows shifted per
+//                 filter tap, zero padding from the TMA out-of-bounds fill (interp.py:69-79)
+//   GradConv2DX   same with the negated shifts and B = W[tap] (interp.py:94-102)
+//   GradConv2DW   M = (tap, c) with per-tap A shifts (interp.py:82-91)
+//
+// Structure (persistent, warp-specialised, one CTA per SM or one CTA pair per TPC):
+//   warp 0      TMA producer: cp.async.bulk.tensor (SWIZZLE_128B / 128B_ATOM_32B) -> smem ring
+//   warp 1      MMA issuer (leader CTA): tcgen05.mma.cta_group::CG.kind::tf32, D in TMEM
+//   warp 2      TMEM allocator (2 accumulators x BN columns: epilogue of tile i overlaps
+//               the mainloop of tile i+1)
+//   warps 4-7   epilogue: tcgen05.ld -> bias / ReLU / GradReLU mask / halo zero -> global
+//   warps 8-11  (3xTF32 only) split each landed stage into big = trunc_tf32(x) and
+//               small = x - big so the MMA warp can issue small*B + A*small + big*big
+// CG = 2 pairs two SMs on one 256 x BN tile (cta_group::2): each CTA stages its own
+// 128 rows of A and half of B, halving per-SM shared-memory operand traffic.
+#pragma once
+
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "../../include/wap_b200.h"
+
+namespace wapgemm {
+
+constexpr int BM = 128;  // rows per CTA
+constexpr int BK = 32;   // fp32 per 128-byte swizzle row
+constexpr int kSmemBudget = 200 * 1024;
+
+struct OperandDev {
+  int32_t mn_major, tap_period, ntaps;
+  int32_t off[WAP_MAX_TAPS];
+};
+
+struct GemmArgs {
+  int64_t M, N;
+  int32_t k_chunks_total, k_chunks_per_split;
+  int32_t m_tiles, n_tiles, splits;  // m_tiles counts cluster tiles (128*CG rows)
+  OperandDev a, b;
+  float* c;
+  int64_t ldc;
+  int64_t split_stride;  // elements between split-K slabs in the workspace
+  float* partial;        // split-K workspace (null when splits == 1)
+  const float* bias;
+  int32_t relu;
+  const float* mask;
+  int64_t ldm;
+  int32_t halo_pad, halo_h, halo_w;
+};
+
+template <int BN, int PREC, int CG>
+struct Cfg {
+  static constexpr int B_ROWS = BN / CG;  // B rows staged by each CTA
+  static constexpr int A_BYTES = BM * BK * 4;
+  static constexpr int B_BYTES = B_ROWS * BK * 4;
+  static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (PREC == 3 ? 2 : 1);
+  static constexpr int STAGES_RAW = kSmemBudget / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512);
+  static constexpr int THREADS = PREC == 3 ? 384 : 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static_assert(STAGES >= 2, "need at least two pipeline stages");
+  static_assert(B_ROWS % 32 == 0, "B rows per CTA must be a multiple of 32");
+};
+
+__device__ __forceinline__ void operand_coords(const OperandDev& op, int mn, int k, int& c0, int& c1) {
+  if (!op.mn_major) {
+    int tap = 0, kin = k;
+    if (op.tap_period > 0) {
+      tap = k / op.tap_period;
+      kin = k - tap * op.tap_period;
+    }
+    c0 = kin;
+    c1 = mn + op.off[tap];
+  } else {
+    int tap = 0, inner = mn;
+    if (op.tap_period > 0) {
+      tap = mn / op.tap_period;
+      if (tap >= op.ntaps) tap = op.ntaps - 1;  // rows past M only feed masked outputs
+      inner = mn - tap * op.tap_period;
+    }
+    c0 = inner;
+    c1 = k + op.off[tap];
+  }
+}
+
+// 2D TMA; for CG == 2 with a leader-side barrier the .cta_group::2 form lets the
+// peer's bytes complete the leader's transaction count.
+template <int CG>
+__device__ __forceinline__ void tma_load(uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0, int c1) {
+  if constexpr (CG == 2) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+  } else {
+    tma_load_2d(dst, tm, bar, c0, c1);
+  }
+}
+
+template <int ROWS, bool MN, int CGT>
+__device__ __forceinline__ void load_operand(const CUtensorMap* tm, const OperandDev& op, uint32_t dst, uint32_t bar,
+                                             int mn0, int k) {
+  if constexpr (!MN) {
+    int c0, c1;
+    operand_coords(op, mn0, k, c0, c1);
+    tma_load<CGT>(dst, tm, bar, c0, c1);  // box {32, ROWS}
+  } else {
+#pragma unroll
+    for (int j = 0; j < ROWS / 32; ++j) {
+      int c0, c1;
+      operand_coords(op, mn0 + 32 * j, k, c0, c1);
+      tma_load<CGT>(dst + j * (BK * 128), tm, bar, c0, c1);  // box {32, BK}
+    }
+  }
+}
+
+template <bool MN>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int kk) {
+  if constexpr (!MN) return make_sdesc_sw128(base + kk * 32, 16, 1024);
+  else return make_sdesc_sw128(base + kk * 1024, BK * 128, 512, 1);
+}
+
+__device__ __forceinline__ void split_tile(uint32_t* raw, uint32_t* small, int nwords, int tid, int nthr) {
+  uint4* r4 = reinterpret_cast<uint4*>(raw);
+  uint4* s4 = reinterpret_cast<uint4*>(small);
+#pragma unroll 4
+  for (int i = tid; i < nwords / 4; i += nthr) {
+    const uint4 x = r4[i];
+    uint4 b, s;
+    b.x = x.x & 0xFFFFE000u;
+    b.y = x.y & 0xFFFFE000u;
+    b.z = x.z & 0xFFFFE000u;
+    b.w = x.w & 0xFFFFE000u;
+    s.x = __float_as_uint(__uint_as_float(x.x) - __uint_as_float(b.x));
+    s.y = __float_as_uint(__uint_as_float(x.y) - __uint_as_float(b.y));
+    s.z = __float_as_uint(__uint_as_float(x.z) - __uint_as_float(b.z));
+    s.w = __float_as_uint(__uint_as_float(x.w) - __uint_as_float(b.w));
+    r4[i] = b;
+    s4[i] = s;
+  }
+}
+
+__device__ __forceinline__ bool halo_row(const GemmArgs& g, int64_t m) {
+  if (g.halo_pad <= 0) return false;
+  const int hp = g.halo_h + 2 * g.halo_pad, wp = g.halo_w + 2 * g.halo_pad;
+  const int w = (int)(m % wp);
+  const int h = (int)((m / wp) % hp);
+  return w < g.halo_pad || w >= g.halo_pad + g.halo_w || h < g.halo_pad || h >= g.halo_pad + g.halo_h;
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Address of the same shared object in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+template <int CG>
+__device__ __forceinline__ void tmem_alloc_cg(uint32_t dst, uint32_t ncols) {
+  if constexpr (CG == 2)
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst), "r"(ncols) : "memory");
+  else
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst), "r"(ncols) : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tmem_relinquish_cg() {
+  if constexpr (CG == 2) asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  else asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr, uint32_t ncols) {
+  if constexpr (CG == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+  else
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void umma_cg(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  if constexpr (CG == 2) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+  } else {
+    umma_tf32(tmem_d, adesc, bdesc, idesc, acc);
+  }
+}
+// Commit: arrive on `bar` in every CTA of the pair once the issued MMAs finish.
+template <int CG>
+__device__ __forceinline__ void umma_commit_cg(uint32_t bar) {
+  if constexpr (CG == 2) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"((uint16_t)3)
+        : "memory");
+  } else {
+    umma_commit(bar);
+  }
+}
+
+struct TileCoord {
+  int m0, n0, split, kc_begin, kc_end;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(const GemmArgs& g, int t, int BNv, int CGv) {
+  TileCoord c;
+  const int n_tile = t % g.n_tiles;
+  const int rest = t / g.n_tiles;
+  const int m_tile = rest % g.m_tiles;
+  c.split = rest / g.m_tiles;
+  c.m0 = m_tile * BM * CGv;
+  c.n0 = n_tile * BNv;
+  c.kc_begin = c.split * g.k_chunks_per_split;
+  c.kc_end = min(g.k_chunks_total, c.kc_begin + g.k_chunks_per_split);
+  return c;
+}
+
+template <int BN, bool A_MN, bool B_MN, int PREC, int CG>
+__global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ GemmArgs g) {
+  using C = Cfg<BN, PREC, CG>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* full_bar = bars;                    // TMA landed (leader-side for CG=2 & TF32)
+  uint64_t* empty_bar = bars + STAGES;          // smem slot free (MMA commit, multicast)
+  uint64_t* conv_bar = bars + 2 * STAGES;       // 3xTF32 split done (leader-side)
+  uint64_t* tfull_bar = bars + 3 * STAGES;      // [2] accumulator ready (MMA commit, multicast)
+  uint64_t* tempty_bar = bars + 3 * STAGES + 2; // [2] accumulator drained (leader-side)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x / CG;
+  const int n_clusters = gridDim.x / CG;
+  const int n_tiles_total = g.m_tiles * g.n_tiles * g.splits;
+
+  auto stage_a = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES); };
+  auto stage_b = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES + C::A_BYTES); };
+  auto stage_as = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES + C::A_BYTES + C::B_BYTES); };
+  auto stage_bs = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES + 2 * C::A_BYTES + C::B_BYTES); };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+      mbar_init(smem_u32(&conv_bar[s]), 128 * CG);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&tfull_bar[i]), 1);
+      mbar_init(smem_u32(&tempty_bar[i]), 128 * CG);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 2) {
+    tmem_alloc_cg<CG>(smem_u32(tmem_holder), C::TMEM_COLS);
+    tmem_relinquish_cg<CG>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs) ----------------
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
+        const TileCoord tc = decode_tile(g, t, BN, CG);
+        const int a_row0 = tc.m0 + (int)rank * BM;
+        const int b_row0 = tc.n0 + (int)rank * C::B_ROWS;
+        for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc) {
+          mbar_wait(smem_u32(&empty_bar[s]), ph ^ 1);
+          uint32_t fb = smem_u32(&full_bar[s]);
+          if constexpr (CG == 2 && PREC == 1) {
+            fb &= 0xFEFFFFFFu;  // the leader's barrier collects both CTAs' bytes
+            if (leader) mbar_arrive_expect_tx(fb, 2 * (C::A_BYTES + C::B_BYTES));
+            load_operand<BM, A_MN, 2>(&tmA, g.a, stage_a(s), fb, a_row0, kc * BK);
+            load_operand<C::B_ROWS, B_MN, 2>(&tmB, g.b, stage_b(s), fb, b_row0, kc * BK);
+          } else {
+            mbar_arrive_expect_tx(fb, C::A_BYTES + C::B_BYTES);
+            load_operand<BM, A_MN, 1>(&tmA, g.a, stage_a(s), fb, a_row0, kc * BK);
+            load_operand<C::B_ROWS, B_MN, 1>(&tmB, g.b, stage_b(s), fb, b_row0, kc * BK);
+          }
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (leader CTA) ----------------
+      constexpr uint32_t idesc = make_idesc_tf32(BM * CG, BN, A_MN, B_MN);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t acc_ph = 0;
+      for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
+        const TileCoord tc = decode_tile(g, t, BN, CG);
+        mbar_wait(smem_u32(&tempty_bar[acc]), acc_ph ^ 1);
+        tc_fence_after();
+        const uint32_t dacc = tmem_base + acc * BN;
+        for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc) {
+          if constexpr (PREC == 3) mbar_wait(smem_u32(&conv_bar[s]), ph);
+          else mbar_wait(smem_u32(&full_bar[s]), ph);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t ad = operand_desc<A_MN>(stage_a(s), kk);
+            const uint64_t bd = operand_desc<B_MN>(stage_b(s), kk);
+            const uint32_t first = (kc > tc.kc_begin || kk > 0) ? 1u : 0u;
+            if constexpr (PREC == 3) {
+              umma_cg<CG>(dacc, operand_desc<A_MN>(stage_as(s), kk), bd, idesc, first);
+              umma_cg<CG>(dacc, ad, operand_desc<B_MN>(stage_bs(s), kk), idesc, 1u);
+              umma_cg<CG>(dacc, ad, bd, idesc, 1u);
+            } else {
+              umma_cg<CG>(dacc, ad, bd, idesc, first);
+            }
+          }
+          umma_commit_cg<CG>(smem_u32(&empty_bar[s]));
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+        umma_commit_cg<CG>(smem_u32(&tfull_bar[acc]));
+        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- epilogue ----------------
+    const int wq = warp - 4;  // TMEM lane quarter
+    const uint32_t tempty_leader = CG == 2 ? map_to_rank(smem_u32(&tempty_bar[0]), 0) : smem_u32(&tempty_bar[0]);
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    const bool vec = (g.ldc % 4) == 0;
+    for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
+      const TileCoord tc = decode_tile(g, t, BN, CG);
+      mbar_wait(smem_u32(&tfull_bar[acc]), acc_ph);
+      tc_fence_after();
+      const int64_t m = (int64_t)tc.m0 + (int64_t)rank * BM + wq * 32 + lane;
+      const bool row_ok = m < g.M;
+      const bool halo = row_ok && halo_row(g, m);
+      const bool raw_out = g.partial != nullptr;
+      float* out_row = raw_out ? g.partial + (int64_t)tc.split * g.split_stride + m * g.ldc : g.c + m * g.ldc;
+      const float* mrow = g.mask ? g.mask + m * g.ldm : nullptr;
+#pragma unroll 1
+      for (int cb = 0; cb < BN / 32; ++cb) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN + cb * 32, v);
+        tmem_ld_wait();
+        const int nb = tc.n0 + cb * 32;
+        if (!row_ok || nb >= g.N) continue;
+        float f[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float x = __uint_as_float(v[j]);
+          const int n = nb + j;
+          if (!raw_out && n < g.N) {
+            if (g.bias) x += __ldg(g.bias + n);
+            if (g.relu) x = fmaxf(x, 0.f);
+            if (mrow) x = (__ldg(mrow + n) > 0.f) ? x : 0.f;
+            if (halo) x = 0.f;
+          }
+          f[j] = x;
+        }
+        if (vec && nb + 32 <= g.N) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(out_row + nb + j) = make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (nb + j < g.N) out_row[nb + j] = f[j];
+        }
+      }
+      tc_fence_before();
+      if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
+      else mbar_arrive(smem_u32(&tempty_bar[acc]));
+      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+  } else if (PREC == 3 && warp >= 8) {
+    // ---------------- 3xTF32 operand split (both CTAs) ----------------
+    const int ct = threadIdx.x - 256;
+    const uint32_t conv_leader = CG == 2 ? map_to_rank(smem_u32(&conv_bar[0]), 0) : smem_u32(&conv_bar[0]);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
+      const TileCoord tc = decode_tile(g, t, BN, CG);
+      for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc) {
+        mbar_wait(smem_u32(&full_bar[s]), ph);
+        uint8_t* base = smem + s * C::STAGE_BYTES;
+        split_tile(reinterpret_cast<uint32_t*>(base), reinterpret_cast<uint32_t*>(base + C::A_BYTES + C::B_BYTES),
+                   BM * BK, ct, 128);
+        split_tile(reinterpret_cast<uint32_t*>(base + C::A_BYTES),
+                   reinterpret_cast<uint32_t*>(base + 2 * C::A_BYTES + C::B_BYTES), C::B_ROWS * BK, ct, 128);
+        fence_proxy_async_smem();
+        if constexpr (CG == 2) mbar_arrive_cluster(conv_leader + s * 8);
+        else mbar_arrive(smem_u32(&conv_bar[s]));
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
+  if (warp == 2) tmem_dealloc_cg<CG>(tmem_base, C::TMEM_COLS);
+}
+
+// Deterministic split-K reduction: fixed slab order, then the epilogue.
+__global__ void splitk_reduce_kernel(const GemmArgs g, int splits);
+
+struct Plan {
+  CUtensorMap tmA, tmB;
+  GemmArgs args;
+  int grid;
+  int bn, a_mn, b_mn, prec, cg, splits;
+};
+
+template <int BN, bool AMN, bool BMN, int PREC, int CG>
+int launch(const Plan& p, cudaStream_t st) {
+  using C = Cfg<BN, PREC, CG>;
+  auto kern = gemm_tc_kernel<BN, AMN, BMN, PREC, CG>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    WAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  int na = 0;
+  if (CG == 2) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    na = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  WAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.args));
+  return WAP_OK;
+}
+
+// dispatch over the three major combinations used on the WAP path
+template <int BN, int PREC, int CG>
+int launch_majors(const Plan& p, cudaStream_t st) {
+  if (!p.a_mn && p.b_mn) return launch<BN, false, true, PREC, CG>(p, st);
+  if (!p.a_mn && !p.b_mn) return launch<BN, false, false, PREC, CG>(p, st);
+  if (p.a_mn && p.b_mn) return launch<BN, true, true, PREC, CG>(p, st);
+  wap_set_error("unsupported operand majors (A MN-major with B K-major)");
+  return WAP_ENOTSUP;
+}
+
+int launch_prec1(const Plan& p, cudaStream_t st);
+int launch_prec3(const Plan& p, cudaStream_t st);
+
+}  // namespace wapgemm

@@ -156,6 +156,65 @@ __global__ void im2col_kernel(const float* __restrict__ x, wap_layout_t xl, int 
   }
 }
 
+// Table-driven im2col: a block owns IM2COL_ROWS output rows; the (u, v, c)
+// decode of every column is computed once per block into shared memory, so the
+// inner loop is a table lookup + one coalesced store per element.
+constexpr int IM2COL_ROWS = 16;
+constexpr int IM2COL_MAXK = 4096;
+
+__global__ void __launch_bounds__(256) im2col_table_kernel(const float* __restrict__ x, wap_layout_t xl, int k, int s,
+                                                           int p, int Ho, int Wo, int P, float* __restrict__ col,
+                                                           int64_t ldcol, int64_t M) {
+  __shared__ short tu[IM2COL_MAXK], tv[IM2COL_MAXK];
+  __shared__ int toff[IM2COL_MAXK];
+  __shared__ int rb[IM2COL_ROWS], rh[IM2COL_ROWS], rw[IM2COL_ROWS];
+  const int C = xl.C;
+  const int K = k * k * C;
+  const int Wxp = xl.W + 2 * xl.pad;
+  for (int kk = threadIdx.x; kk < K; kk += blockDim.x) {
+    const int c = kk % C, t = kk / C;
+    const int u = t / k, v = t % k;
+    tu[kk] = (short)u;
+    tv[kk] = (short)v;
+    toff[kk] = (u * Wxp + v) * xl.ld + c;
+  }
+  const int Hp = Ho + 2 * P, Wp = Wo + 2 * P;
+  for (int64_t r0 = (int64_t)blockIdx.x * IM2COL_ROWS; r0 < M; r0 += (int64_t)gridDim.x * IM2COL_ROWS) {
+    __syncthreads();
+    if (threadIdx.x < IM2COL_ROWS) {
+      const int64_t m = r0 + threadIdx.x;
+      int b = -1, ho = -1, wo = -1;
+      if (m < M) {
+        wo = (int)(m % Wp) - P;
+        const int64_t q = m / Wp;
+        ho = (int)(q % Hp) - P;
+        b = (int)(q / Hp);
+        if (ho < 0 || ho >= Ho || wo < 0 || wo >= Wo) b = -2;  // halo row -> zeros
+      }
+      rb[threadIdx.x] = b;
+      rh[threadIdx.x] = ho * s - p;
+      rw[threadIdx.x] = wo * s - p;
+    }
+    __syncthreads();
+    for (int i = 0; i < IM2COL_ROWS; ++i) {
+      const int64_t m = r0 + i;
+      if (m >= M) break;
+      const int b = rb[i], h0 = rh[i], w0 = rw[i];
+      float* out = col + m * ldcol;
+      // base address of tap (0,0) channel 0 (may be outside; guarded per element)
+      const int64_t base = (((int64_t)(b < 0 ? 0 : b) * (xl.H + 2 * xl.pad) + h0 + xl.pad) * Wxp + w0 + xl.pad) * xl.ld;
+      for (int kk = threadIdx.x; kk < ldcol; kk += blockDim.x) {
+        float v = 0.f;
+        if (b >= 0 && kk < K) {
+          const int hi = h0 + tu[kk], wi = w0 + tv[kk];
+          if (hi >= 0 && hi < xl.H && wi >= 0 && wi < xl.W) v = __ldg(x + base + toff[kk]);
+        }
+        out[kk] = v;
+      }
+    }
+  }
+}
+
 __global__ void col2im_kernel(const float* __restrict__ dcol, int64_t ldcol, int k, int s, int p, int Ho, int Wo,
                               int P, float* __restrict__ dx, wap_layout_t dl, const float* __restrict__ mask,
                               wap_layout_t ml) {
@@ -376,6 +435,114 @@ __global__ void lrn_bwd_kernel(const float* __restrict__ x, wap_layout_t xl, con
   }
 }
 
+// Fast LRN for compact channels (ld == C, C % 4 == 0, C4 = C/4 known at compile
+// time): float4 tile loads into shared memory, per-pixel decode once, fast
+// log2/exp2 power. `PIX` pixels per block iteration.
+__device__ __forceinline__ float lrn_pow(float s, float e) { return exp2f(e * __log2f(s)); }
+
+template <int C4, int PIX, bool BWD>
+__global__ void __launch_bounds__(256) lrn_fast_kernel(const float* __restrict__ x, wap_layout_t xl,
+                                                       const float* __restrict__ dy, wap_layout_t dyl, int size,
+                                                       float alpha, float beta, float k, float* __restrict__ out,
+                                                       wap_layout_t ol, const float* __restrict__ mask,
+                                                       wap_layout_t ml) {
+  constexpr int C = C4 * 4;
+  __shared__ float4 sx[PIX * C4];
+  __shared__ float4 sd[BWD ? PIX * C4 : 1];
+  __shared__ float st[BWD ? PIX * C : 1];
+  __shared__ int64_t px[PIX], pd[BWD ? PIX : 1], po[PIX], pm[BWD ? PIX : 1];
+  const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
+  const int half = size / 2;
+  for (int64_t p0 = (int64_t)blockIdx.x * PIX; p0 < npix; p0 += (int64_t)gridDim.x * PIX) {
+    __syncthreads();
+    if (threadIdx.x < PIX) {
+      int64_t p = p0 + threadIdx.x;
+      if (p >= npix) p = npix - 1;
+      int b, h, w;
+      pixel_of(xl, p, b, h, w);
+      px[threadIdx.x] = lidx(xl, b, h, w, 0);
+      po[threadIdx.x] = lidx(ol, b, h, w, 0);
+      if (BWD) {
+        pd[threadIdx.x] = lidx(dyl, b, h, w, 0);
+        pm[threadIdx.x] = mask ? lidx(ml, b, h, w, 0) : 0;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < PIX * C4; i += blockDim.x) {
+      const int pi = i / C4, c4 = i % C4;
+      sx[i] = *reinterpret_cast<const float4*>(x + px[pi] + 4 * c4);
+      if (BWD) sd[i] = *reinterpret_cast<const float4*>(dy + pd[pi] + 4 * c4);
+    }
+    __syncthreads();
+    const float* fx = reinterpret_cast<const float*>(sx);
+    if (BWD) {
+      const float* fd = reinterpret_cast<const float*>(sd);
+      for (int i = threadIdx.x; i < PIX * C; i += blockDim.x) {
+        const int pi = i / C, c = i % C;
+        const float* row = fx + pi * C;
+        float ss = 0.f;
+        for (int j = max(0, c - half); j <= min(C - 1, c + half); ++j) ss += row[j] * row[j];
+        const float s = k + alpha * ss;
+        st[i] = fd[i] * row[c] * lrn_pow(s, -beta - 1.f);
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < PIX * C4; i += blockDim.x) {
+      const int pi = i / C4, c0 = (i % C4) * 4;
+      if (p0 + pi >= npix) continue;
+      const float* row = fx + pi * C;
+      float o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + j;
+        float ss = 0.f;
+        for (int q = max(0, c - half); q <= min(C - 1, c + half); ++q) ss += row[q] * row[q];
+        const float s = k + alpha * ss;
+        if (!BWD) {
+          o[j] = row[c] * lrn_pow(s, -beta);
+        } else {
+          const float* trow = st + pi * C;
+          float acc = 0.f;
+          for (int q = max(0, c - half); q <= min(C - 1, c + half); ++q) acc += trow[q];
+          const float* drow = reinterpret_cast<const float*>(sd) + pi * C;
+          o[j] = drow[c] * lrn_pow(s, -beta) - 2.f * alpha * beta * row[c] * acc;
+        }
+      }
+      if (BWD && mask) {
+        const float4 m = *reinterpret_cast<const float4*>(mask + pm[pi] + c0);
+        if (!(m.x > 0.f)) o[0] = 0.f;
+        if (!(m.y > 0.f)) o[1] = 0.f;
+        if (!(m.z > 0.f)) o[2] = 0.f;
+        if (!(m.w > 0.f)) o[3] = 0.f;
+      }
+      *reinterpret_cast<float4*>(out + po[pi] + c0) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+template <bool BWD>
+bool launch_lrn_fast(const float* x, wap_layout_t xl, const float* dy, wap_layout_t dyl, int size, float alpha,
+                     float beta, float bias, float* out, wap_layout_t ol, const float* mask, wap_layout_t ml,
+                     cudaStream_t st) {
+  const bool compact = xl.ld == xl.C && ol.ld == xl.C && (!BWD || dyl.ld == xl.C) && (!mask || ml.ld == xl.C);
+  if (!compact) return false;
+  const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
+  auto blocks = [&](int pix) { return grid_for(npix, pix); };
+  if (xl.C == 64) {
+    lrn_fast_kernel<16, 32, BWD><<<blocks(32), 256, 0, st>>>(x, xl, dy, dyl, size, alpha, beta, bias, out, ol, mask, ml);
+    return true;
+  }
+  if (xl.C == 192) {
+    lrn_fast_kernel<48, 16, BWD><<<blocks(16), 256, 0, st>>>(x, xl, dy, dyl, size, alpha, beta, bias, out, ol, mask, ml);
+    return true;
+  }
+  if (xl.C == 96) {
+    lrn_fast_kernel<24, 16, BWD><<<blocks(16), 256, 0, st>>>(x, xl, dy, dyl, size, alpha, beta, bias, out, ol, mask, ml);
+    return true;
+  }
+  return false;
+}
+
 // ---------------------------------------------------------------------------
 // softmax cross-entropy (+ gradient): one block per row
 // ---------------------------------------------------------------------------
@@ -541,9 +708,17 @@ extern "C" int wap_im2col(const float* x, wap_layout_t xl, int k, int stride, in
   if ((rc = check_layout(xl, "x"))) return rc;
   WAP_CHECK_ARG(k >= 1 && stride >= 1 && padding >= 0 && Ho >= 1 && Wo >= 1 && out_pad >= 0, "im2col: bad geometry");
   WAP_CHECK_ARG(ldcol >= (int64_t)k * k * xl.C, "im2col: ldcol too small");
-  const int64_t total = (int64_t)xl.B * (Ho + 2 * out_pad) * (Wo + 2 * out_pad) * ldcol;
-  im2col_kernel<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(x, xl, k, stride, padding, Ho, Wo, out_pad, col,
-                                                                 ldcol);
+  const int64_t M = (int64_t)xl.B * (Ho + 2 * out_pad) * (Wo + 2 * out_pad);
+  const int64_t total = M * ldcol;
+  if ((int64_t)k * k * xl.C <= IM2COL_MAXK) {
+    int64_t blocks = (M + IM2COL_ROWS - 1) / IM2COL_ROWS;
+    if (blocks > WAP_NUM_SMS * 32) blocks = WAP_NUM_SMS * 32;
+    im2col_table_kernel<<<(int)blocks, 256, 0, STREAM(stream)>>>(x, xl, k, stride, padding, Ho, Wo, out_pad, col,
+                                                                ldcol, M);
+  } else {
+    im2col_kernel<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(x, xl, k, stride, padding, Ho, Wo, out_pad, col,
+                                                                   ldcol);
+  }
   WAP_LAUNCH_CHECK();
   COUNT_LAUNCH();
   return WAP_OK;
@@ -601,7 +776,8 @@ extern "C" int wap_lrn_fwd(const float* x, wap_layout_t xl, int size, float alph
   WAP_CHECK_ARG(size >= 1 && size % 2 == 1, "LRN size must be odd");
   const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
   const int smem = LRN_PIX * xl.C * 4;
-  lrn_fwd_kernel<<<grid_for(npix, LRN_PIX), 256, smem, STREAM(stream)>>>(x, xl, size, alpha, beta, bias, y, yl);
+  if (!launch_lrn_fast<false>(x, xl, nullptr, xl, size, alpha, beta, bias, y, yl, nullptr, xl, STREAM(stream)))
+    lrn_fwd_kernel<<<grid_for(npix, LRN_PIX), 256, smem, STREAM(stream)>>>(x, xl, size, alpha, beta, bias, y, yl);
   WAP_LAUNCH_CHECK();
   COUNT_LAUNCH();
   return WAP_OK;
@@ -615,8 +791,9 @@ extern "C" int wap_lrn_bwd(const float* x, wap_layout_t xl, const float* dy, wap
   if (mask && (rc = check_layout(ml, "mask"))) return rc;
   const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
   const int smem = 4 * LRN_PIX * xl.C * 4;
-  lrn_bwd_kernel<<<grid_for(npix, LRN_PIX), 256, smem, STREAM(stream)>>>(x, xl, dy, dyl, size, alpha, beta, bias,
-                                                                         dx, dxl, mask, ml);
+  if (!launch_lrn_fast<true>(x, xl, dy, dyl, size, alpha, beta, bias, dx, dxl, mask, ml, STREAM(stream)))
+    lrn_bwd_kernel<<<grid_for(npix, LRN_PIX), 256, smem, STREAM(stream)>>>(x, xl, dy, dyl, size, alpha, beta, bias,
+                                                                           dx, dxl, mask, ml);
   WAP_LAUNCH_CHECK();
   COUNT_LAUNCH();
   return WAP_OK;

@@ -31,7 +31,13 @@ def test_fc_forward(cuda, prec, M, Nn, Kk):
     K.gemm(x, w, y, a_mn=False, b_mn=True, M=M, Nn=Nn, K=Kk, bias=bias, relu=True, precision=prec)
     torch.cuda.synchronize()
     ref = torch.relu(x.double() @ w.double() + bias.double())
-    assert dev(y, ref) < TOL[prec]
+    tol = TOL[prec]
+    if prec == 3:
+        # fp32-accurate means: no worse than a few times an fp32 CUDA-core GEMM
+        torch.backends.cuda.matmul.allow_tf32 = False
+        fp32_err = dev(torch.relu(x @ w + bias), ref)
+        tol = max(tol, 4 * fp32_err)
+    assert dev(y, ref) < tol
 
 
 @pytest.mark.parametrize("prec", [1, 3])

@@ -30,7 +30,8 @@ def main():
     tp = trainer.plan_training(g, 1, planner.load_profile("b200"), force_d=1)
     tr = trainer.Trainer(tp, precision=args.precision, use_graph=False, variables=he_init(g))
     tr.load(synthetic_batch(g, 0, args.batch))
-    tr.run()
+    if not args.only:
+        tr.run()
     torch.cuda.synchronize()
     sel = [s for s in tr.prog.steps if args.only in s.name]
     print("selected:", [s.name for s in sel], flush=True)
