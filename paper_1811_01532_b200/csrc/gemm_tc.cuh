@@ -53,20 +53,106 @@ struct GemmArgs {
   int32_t halo_pad, halo_h, halo_w;
 };
 
+// 3xTF32 keeps the A operand in TMEM (tcgen05 "TS" form): the splitter warps
+// read each landed A row once from shared memory and store big/small halves
+// into TMEM with tcgen05.st, so the three MMAs per k-step read only B from
+// shared memory. Layout of the 512 TMEM columns for PREC == 3:
+//   [0, ACC_BUFS*BN)                accumulators
+//   [A_COL0 + s*64, +32)            A big  of stage s   (lane = row, column = k)
+//   [A_COL0 + s*64 + 32, +32)       A small of stage s
 template <int BN, int PREC, int CG>
 struct Cfg {
   static constexpr int B_ROWS = BN / CG;  // B rows staged by each CTA
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = B_ROWS * BK * 4;
-  static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (PREC == 3 ? 2 : 1);
-  static constexpr int STAGES_RAW = kSmemBudget / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512);
-  static constexpr int THREADS = PREC == 3 ? 384 : 256;
+  // PREC 3 smem stage: A raw | B raw | B small
+  static constexpr int STAGE_BYTES = PREC == 3 ? (A_BYTES + 2 * B_BYTES) : (A_BYTES + B_BYTES);
+  // two accumulators (epilogue overlap) only if >= 4 A stages still fit in TMEM
+  static constexpr int ACC_BUFS = (PREC == 3 && 512 - 2 * BN < 4 * 64) ? 1 : 2;
+  static constexpr int A_COL0 = ACC_BUFS * BN;
+  static constexpr int TMEM_A_SLOTS = PREC == 3 ? (512 - A_COL0) / 64 : 64;
+  static constexpr int STAGES_SMEM = kSmemBudget / STAGE_BYTES;
+  static constexpr int STAGES_A = STAGES_SMEM < TMEM_A_SLOTS ? STAGES_SMEM : TMEM_A_SLOTS;
+  static constexpr int STAGES = STAGES_A > 8 ? 8 : STAGES_A;
+  static constexpr int TMEM_COLS = PREC == 3 ? 512 : ((2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512));
+  static constexpr int THREADS = PREC == 3 ? 512 : 256;  // + 2 x 4 splitter warps
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
   static_assert(STAGES >= 2, "need at least two pipeline stages");
   static_assert(B_ROWS % 32 == 0, "B rows per CTA must be a multiple of 32");
 };
+
+// A row m (32 k-values) of a landed stage, K-major SWIZZLE_128B tile.
+__device__ __forceinline__ void load_a_row_kmajor(const uint8_t* tile, int m, uint32_t (&v)[32]) {
+  const uint8_t* row = tile + m * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint4 q = *reinterpret_cast<const uint4*>(row + ((j ^ (m & 7)) << 4));
+    v[4 * j] = q.x;
+    v[4 * j + 1] = q.y;
+    v[4 * j + 2] = q.z;
+    v[4 * j + 3] = q.w;
+  }
+}
+
+// A column m (32 k-values) of an MN-major tile: 4 blocks of [32 k][32 m] with the
+// 32B-atom swizzle (32-byte chunk index XOR (k & 3)).
+__device__ __forceinline__ void load_a_row_mnmajor(const uint8_t* tile, int m, uint32_t (&v)[32]) {
+  const uint8_t* blk = tile + (m >> 5) * (BK * 128);
+  const int mi = m & 31;
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    v[k] = *reinterpret_cast<const uint32_t*>(blk + k * 128 + ((((mi >> 3) ^ (k & 3))) << 5) + (mi & 7) * 4);
+}
+
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] * B[smem]
+template <int CG>
+__device__ __forceinline__ void umma_ts_cg(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t acc) {
+  if constexpr (CG == 2) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+  }
+}
+
+// small = x - trunc13(x) for the B tile (big is the raw word: kind::tf32 ignores
+// the low 13 mantissa bits, measured bitwise by tools/trunc_probe.py).
+__device__ __forceinline__ void split_small_only(const uint32_t* raw, uint32_t* small, int nwords, int tid, int nthr) {
+  const uint4* r4 = reinterpret_cast<const uint4*>(raw);
+  uint4* s4 = reinterpret_cast<uint4*>(small);
+#pragma unroll 4
+  for (int i = tid; i < nwords / 4; i += nthr) {
+    const uint4 x = r4[i];
+    uint4 s;
+    s.x = __float_as_uint(__uint_as_float(x.x) - __uint_as_float(x.x & 0xFFFFE000u));
+    s.y = __float_as_uint(__uint_as_float(x.y) - __uint_as_float(x.y & 0xFFFFE000u));
+    s.z = __float_as_uint(__uint_as_float(x.z) - __uint_as_float(x.z & 0xFFFFE000u));
+    s.w = __float_as_uint(__uint_as_float(x.w) - __uint_as_float(x.w & 0xFFFFE000u));
+    s4[i] = s;
+  }
+}
 
 __device__ __forceinline__ void operand_coords(const OperandDev& op, int mn, int k, int& c0, int& c1) {
   if (!op.mn_major) {
@@ -260,8 +346,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
 
   auto stage_a = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES); };
   auto stage_b = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES + C::A_BYTES); };
-  auto stage_as = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES + C::A_BYTES + C::B_BYTES); };
-  auto stage_bs = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES + 2 * C::A_BYTES + C::B_BYTES); };
+  auto stage_bs = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES + C::A_BYTES + C::B_BYTES); };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -269,11 +354,11 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(&full_bar[s]), 1);
       mbar_init(smem_u32(&empty_bar[s]), 1);
-      mbar_init(smem_u32(&conv_bar[s]), 128 * CG);
+      mbar_init(smem_u32(&conv_bar[s]), 4 * CG);  // one arrive per splitter warp
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&tfull_bar[i]), 1);
-      mbar_init(smem_u32(&tempty_bar[i]), 128 * CG);
+      mbar_init(smem_u32(&tempty_bar[i]), 4 * CG);  // one arrive per epilogue warp
     }
     mbar_fence_init();
   }
@@ -316,7 +401,8 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ---------------- MMA issuer (leader CTA) ----------------
-      constexpr uint32_t idesc = make_idesc_tf32(BM * CG, BN, A_MN, B_MN);
+      // A lives in TMEM (K-major by construction) for 3xTF32
+      constexpr uint32_t idesc = make_idesc_tf32(BM * CG, BN, PREC == 3 ? false : A_MN, B_MN);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -332,22 +418,22 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint64_t ad = operand_desc<A_MN>(stage_a(s), kk);
             const uint64_t bd = operand_desc<B_MN>(stage_b(s), kk);
             const uint32_t first = (kc > tc.kc_begin || kk > 0) ? 1u : 0u;
             if constexpr (PREC == 3) {
-              umma_cg<CG>(dacc, operand_desc<A_MN>(stage_as(s), kk), bd, idesc, first);
-              umma_cg<CG>(dacc, ad, operand_desc<B_MN>(stage_bs(s), kk), idesc, 1u);
-              umma_cg<CG>(dacc, ad, bd, idesc, 1u);
+              const uint32_t a_big = tmem_base + C::A_COL0 + s * 64 + kk * 8;
+              umma_ts_cg<CG>(dacc, a_big + 32, bd, idesc, first);                          // small * B
+              umma_ts_cg<CG>(dacc, a_big, operand_desc<B_MN>(stage_bs(s), kk), idesc, 1u);  // A * small
+              umma_ts_cg<CG>(dacc, a_big, bd, idesc, 1u);                                   // big * big
             } else {
-              umma_cg<CG>(dacc, ad, bd, idesc, first);
+              umma_cg<CG>(dacc, operand_desc<A_MN>(stage_a(s), kk), bd, idesc, first);
             }
           }
           umma_commit_cg<CG>(smem_u32(&empty_bar[s]));
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
         umma_commit_cg<CG>(smem_u32(&tfull_bar[acc]));
-        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+        if (++acc == C::ACC_BUFS) { acc = 0; acc_ph ^= 1; }
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -398,28 +484,55 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
         }
       }
       tc_fence_before();
-      if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
-      else mbar_arrive(smem_u32(&tempty_bar[acc]));
-      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
+        else mbar_arrive(smem_u32(&tempty_bar[acc]));
+      }
+      if (++acc == C::ACC_BUFS) { acc = 0; acc_ph ^= 1; }
     }
   } else if (PREC == 3 && warp >= 8) {
     // ---------------- 3xTF32 operand split (both CTAs) ----------------
-    const int ct = threadIdx.x - 256;
+    // Two groups of 4 warps alternate stages (two stages in flight). Within a
+    // group, thread ct owns row ct of the CTA's A tile = TMEM lane ct.
+    const int group = (warp - 8) >> 2;
+    const int ct = (threadIdx.x - 256) & 127;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t conv_leader = CG == 2 ? map_to_rank(smem_u32(&conv_bar[0]), 0) : smem_u32(&conv_bar[0]);
     int s = 0;
     uint32_t ph = 0;
+    int it = 0;
     for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
       const TileCoord tc = decode_tile(g, t, BN, CG);
-      for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc) {
+      for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc, ++it) {
+        if ((it & 1) != group) {
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+          continue;
+        }
         mbar_wait(smem_u32(&full_bar[s]), ph);
         uint8_t* base = smem + s * C::STAGE_BYTES;
-        split_tile(reinterpret_cast<uint32_t*>(base), reinterpret_cast<uint32_t*>(base + C::A_BYTES + C::B_BYTES),
-                   BM * BK, ct, 128);
-        split_tile(reinterpret_cast<uint32_t*>(base + C::A_BYTES),
-                   reinterpret_cast<uint32_t*>(base + 2 * C::A_BYTES + C::B_BYTES), C::B_ROWS * BK, ct, 128);
+        uint32_t v[32], w[32];
+        if constexpr (A_MN) load_a_row_mnmajor(base, ct, v);
+        else load_a_row_kmajor(base, ct, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const uint32_t big = v[j] & 0xFFFFE000u;
+          w[j] = __float_as_uint(__uint_as_float(v[j]) - __uint_as_float(big));
+          v[j] = big;
+        }
+        const uint32_t acol = tmem_base + lane_base + C::A_COL0 + s * 64;
+        tmem_st_32x32b_x32(acol, v);
+        tmem_st_32x32b_x32(acol + 32, w);
+        split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_BYTES),
+                         reinterpret_cast<uint32_t*>(base + C::A_BYTES + C::B_BYTES), C::B_ROWS * BK, ct, 128);
+        tmem_st_wait();
+        tc_fence_before();
         fence_proxy_async_smem();
-        if constexpr (CG == 2) mbar_arrive_cluster(conv_leader + s * 8);
-        else mbar_arrive(smem_u32(&conv_bar[s]));
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_cluster(conv_leader + s * 8);
+          else mbar_arrive(smem_u32(&conv_bar[s]));
+        }
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }

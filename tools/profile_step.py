@@ -33,7 +33,8 @@ def main():
     if not args.only:
         tr.run()
     torch.cuda.synchronize()
-    sel = [s for s in tr.prog.steps if args.only in s.name]
+    names = args.only.split(",")
+    sel = [s for s in tr.prog.steps if s.name in names] or [s for s in tr.prog.steps if args.only in s.name]
     print("selected:", [s.name for s in sel], flush=True)
     for _ in range(args.reps):
         for s in sel:
