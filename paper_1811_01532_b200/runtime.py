@@ -154,8 +154,12 @@ class Program:
     """
 
     def __init__(self, graph: Graph, precision: int = 3, device=None, in_place: bool = False,
-                 collective=None):
+                 collective=None, bucket_bytes: int = 64 << 20):
         import torch
+
+        self._collectives: list = []
+        self.bucket_bytes = bucket_bytes
+        self.buckets: list = []
 
         self.torch = torch
         self.L = N.lib()
@@ -528,8 +532,64 @@ class Program:
                 self._lower_sgd(n)
             else:
                 raise EvalError(f"no GPU rule for kind {k.value}")
+        self._schedule_collectives()
+        self._fuse_updates()
         self.steps.extend(self.update_steps)
         self.update_steps = []
+
+    def _schedule_collectives(self) -> None:
+        """Bucket the rank-local gradient allreduces and overlap them with backward.
+
+        Gradients live in one arena in readiness order, so a bucket is a
+        contiguous slice. Each bucket's allreduce is issued on a side stream as
+        soon as its last gradient is produced (event on the compute stream), while
+        the remaining backward kernels keep running; a join step makes the
+        compute stream wait for the side stream before the SGD update."""
+        if not self._collectives:
+            return
+        items = sorted(self._collectives, key=lambda x: x[0])
+        base = self.grad_arena.data_ptr()
+        buckets: list[list] = []
+        for ready, nid, t in items:
+            lo = (t.ptr - base) // 4
+            hi = lo + t.numel_storage()
+            if buckets:
+                b = buckets[-1]
+                adjacent = lo == b[2] or hi == b[1]
+                if adjacent and (max(hi, b[2]) - min(lo, b[1])) * 4 <= self.bucket_bytes:
+                    b[0] = max(b[0], ready)
+                    b[1], b[2] = min(lo, b[1]), max(hi, b[2])
+                    b[3].append(nid)
+                    continue
+            buckets.append([ready, lo, hi, [nid]])
+        side = self.torch.cuda.Stream(device=self.device)
+        self.comm_stream = side
+        inserts: dict[int, list] = {}
+        for ready, lo, hi, ids in buckets:
+            inserts.setdefault(ready, []).append(
+                _BucketStep("+".join(ids), self.collective, self.grad_arena[lo:hi], side, self.torch))
+        new_steps = []
+        for i, st in enumerate(self.steps):
+            new_steps.extend(inserts.get(i, []))
+            new_steps.append(st)
+        new_steps.extend(inserts.get(len(self.steps), []))
+        new_steps.append(_JoinStep(side, self.torch))
+        self.steps = new_steps
+        self.buckets = [(lo * 4, hi * 4, ids) for _, lo, hi, ids in buckets]
+
+    def _fuse_updates(self) -> None:
+        """In-place training: one SGD launch over the whole variable arena when all
+        updates share a learning rate (variables without an update have a zero
+        gradient slot, so w - lr*0 leaves them unchanged)."""
+        if not self.in_place or not self.update_steps:
+            return
+        lrs = {float(self.node(u).attr("learning_rate")) for u in self.updates}
+        if len(lrs) != 1 or any(not isinstance(s, Step) for s in self.update_steps):
+            return
+        lr = lrs.pop()
+        self.update_steps = [Step("sgd(arena)", self.L.wap_sgd,
+                                  (self.var_arena.data_ptr(), self.grad_arena.data_ptr(), C.c_float(lr),
+                                   self.var_arena.data_ptr(), self.arena_numel), "SgdUpdate (fused arena)")]
 
     # -- tensor access ---------------------------------------------------------
     def _in(self, consumer: Node, nid: str) -> Tensor:
@@ -818,10 +878,11 @@ class Program:
         if len(n.inputs) >= 2:  # all replicas in this process: left fold (interp.py:181-182)
             self._lower_add_n(n)
             return
-        # rank-local view: the sum crosses processes
+        # rank-local view: the sum crosses processes. Recorded here, bucketed in
+        # _schedule_collectives once every producer's position is known.
         src = self._in(n, n.inputs[0])
         if self.collective is not None:
-            self.steps.append(_CollectiveStep(n.id, self.collective, src))
+            self._collectives.append((len(self.steps), n.id, src))
 
     def _lower_concat(self, n: Node) -> None:
         out = self._out(n.id)
@@ -942,10 +1003,31 @@ class Program:
 
 
 class _CollectiveStep:
-    def __init__(self, name, fn, t: Tensor):
+    """Marker base for steps that call into a cross-process collective."""
+
+
+class _BucketStep(_CollectiveStep):
+    def __init__(self, name, fn, buf, side, torch):
         self.name = name
         self.fn = fn
-        self.t = t
+        self.buf = buf
+        self.side = side
+        self.torch = torch
 
     def __call__(self, stream: int) -> None:
-        self.fn(self.t.buf)
+        torch = self.torch
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.side.wait_event(ev)
+        with torch.cuda.stream(self.side):
+            self.fn(self.buf)
+
+
+class _JoinStep(_CollectiveStep):
+    def __init__(self, side, torch):
+        self.name = "join(comm)"
+        self.side = side
+        self.torch = torch
+
+    def __call__(self, stream: int) -> None:
+        self.torch.cuda.current_stream().wait_stream(self.side)

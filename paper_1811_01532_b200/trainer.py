@@ -101,7 +101,8 @@ class Trainer:
     by the global batch, so no 1/N scaling is needed (training.py:94-102)."""
 
     def __init__(self, tplan: TrainingPlan, rank: int = 0, precision: int = 3, seed: int = 0,
-                 variables: dict | None = None, process_group=None, use_graph: bool = True):
+                 variables: dict | None = None, process_group=None, use_graph: bool = True,
+                 bucket_bytes: int = 64 << 20):
         import torch
 
         from .interp import initial_variables
@@ -114,7 +115,8 @@ class Trainer:
         self.view = rank_view(tplan.graph, rank, self.d)
         self.pg = process_group
         collective = self._allreduce if self.d > 1 else None
-        self.prog = Program(self.view, precision=precision, in_place=True, collective=collective)
+        self.prog = Program(self.view, precision=precision, in_place=True, collective=collective,
+                            bucket_bytes=bucket_bytes)
         init = initial_variables(self.view, seed)
         if variables:
             for k in init:

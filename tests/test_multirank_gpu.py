@@ -1,0 +1,98 @@
+"""Two ranks on one B200 (gloo on CUDA tensors): each rank runs its rank view of
+the WAP-transformed graph through Trainer (bucketed allreduce on a side stream,
+fused arena SGD, in-place variables). The updated variables and per-rank losses
+must match a single-process GPU execution of the full transformed graph."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _bindings(graph, seed=3):
+    rs = np.random.default_rng(seed)
+    out = {}
+    for n in graph:
+        shape = tuple(n.attr("shape") or ())
+        if n.kind.value == "Variable":
+            fan = int(np.prod(shape[:-1])) if len(shape) > 1 else 1
+            out[n.id] = (np.sqrt(2.0 / fan) if len(shape) > 1 else 0.01) * rs.standard_normal(shape)
+        elif n.id == "labels":
+            lab = np.zeros(shape)
+            lab[np.arange(shape[0]), rs.integers(0, shape[1], shape[0])] = 1
+            out[n.id] = lab
+        elif n.kind.value == "Input":
+            out[n.id] = rs.standard_normal(shape)
+    return out
+
+
+def _worker(rank, world, port, net, kw, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_1811_01532_b200 import models, planner, trainer
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = models.MODELS[net](**kw)
+        bind = _bindings(g)
+        tp = trainer.plan_training(g, world, planner.load_profile("b200"), force_d=world)
+        tr = trainer.Trainer(tp, rank=rank, variables={k: v for k, v in bind.items() if k not in ("images", "labels")},
+                             bucket_bytes=1 << 20)
+        b = kw["batch"] // world
+        shard = {k: torch.from_numpy(np.ascontiguousarray(bind[k][rank * b:(rank + 1) * b]).astype(np.float32))
+                 for k in ("images", "labels")}
+        loss = tr.step(shard, fetch=True)
+        q.put((rank, loss, tr.variables(), len(tr.prog.buckets)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("net,kw", [("alexnet_like", {"batch": 16}), ("alexnet", {"batch": 4, "image": 99})])
+def test_two_ranks_match_single_process(cuda, net, kw):
+    from paper_1811_01532_b200 import graph_modifier as gm
+    from paper_1811_01532_b200 import interp, models, planner
+    from oracle import interp_ref as O
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, net, kw, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, loss, var, nb = q.get(timeout=600)
+        res[r] = (loss, var, nb)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    g = models.MODELS[net](**kw)
+    bind = _bindings(g)
+    tg = gm.transform(g, planner.ParallelPlan(world, tuple(range(world)), (), 0.0))[0]
+    full = dict(bind)
+    for n in tg:
+        if n.kind.value == "Variable" and n.id not in full:
+            full[n.id] = bind[n.id.split("/dev")[0]]
+    ref = interp.execute(tg, full, 0)
+    for rank, (loss, var, nb) in res.items():
+        assert nb >= (2 if net == "alexnet" else 1), "expected several allreduce buckets"
+        assert abs(loss - ref[f"loss/dev{rank}"][0]) <= 1e-4 * max(1.0, abs(loss))
+        for vid, val in var.items():
+            upd = vid.replace(f"/dev{rank}", f"_upd/dev{rank}")
+            assert O.relative_deviation(val, ref[upd]) < 1e-5, vid
