@@ -69,7 +69,8 @@ typedef struct {
   int32_t halo_pad, halo_h, halo_w; /* unpadded H, W of the grid */
   int32_t precision;                /* 1 = TF32, 3 = 3xTF32 (fp32-accurate) */
   int32_t splits;                   /* split-K factor, 0 = automatic */
-  int32_t block_n;                  /* 0 = automatic, else 64/128/256 */
+  int32_t block_n;                  /* 0 = automatic, else 64/128/192/256 */
+  int32_t cluster;                  /* 0 = automatic, 1 = one CTA, 2 = CTA pair (cta_group::2) */
   float* workspace;                 /* split-K partials, wap_gemm_workspace_bytes() */
   int64_t workspace_bytes;
 } wap_gemm_desc_t;

@@ -87,9 +87,11 @@ Shape plan_shape(const wap_gemm_desc_t& d) {
   s.n_tiles = wap_ceil_div(d.N, s.bn);
   // CTA pairs (cta_group::2) whenever there are enough 256-row tiles to fill the pairs
   const long long pair_tiles = (long long)wap_ceil_div(d.M, 2 * BM) * s.n_tiles;
-  s.cg = (d.M > BM && pair_tiles >= WAP_NUM_SMS / 4) ? 2 : 1;
+  s.cg = (d.M > BM && (pair_tiles >= WAP_NUM_SMS / 4 || d.K >= 64 * BK)) ? 2 : 1;
+  if (d.cluster == 1 || d.cluster == 2) s.cg = d.cluster;
   const char* force = getenv("WAP_GEMM_CG");
   if (force) s.cg = atoi(force) == 2 ? 2 : 1;
+  if (d.M <= BM) s.cg = 1;
   s.m_tiles = wap_ceil_div(d.M, BM * s.cg);
   const long long tiles = (long long)s.m_tiles * s.n_tiles;
   const long long slots = WAP_NUM_SMS / s.cg;

@@ -30,7 +30,8 @@ namespace wapgemm {
 
 constexpr int BM = 128;  // rows per CTA
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kSmemBudget = 204 * 1024;  // + 16.5 KB epilogue staging below
+constexpr int kEpiStage = 4 * 32 * 33 * 4;
 
 struct OperandDev {
   int32_t mn_major, tap_period, ntaps;
@@ -76,7 +77,7 @@ struct Cfg {
   static constexpr int STAGES = STAGES_A > 8 ? 8 : STAGES_A;
   static constexpr int TMEM_COLS = PREC == 3 ? 512 : ((2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512));
   static constexpr int THREADS = PREC == 3 ? 512 : 256;  // + 2 x 4 splitter warps
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + kEpiStage;
   static_assert(STAGES >= 2, "need at least two pipeline stages");
   static_assert(B_ROWS % 32 == 0, "B rows per CTA must be a multiple of 32");
 };
@@ -439,6 +440,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
   } else if (warp >= 4 && warp < 8) {
     // ---------------- epilogue ----------------
     const int wq = warp - 4;  // TMEM lane quarter
+    float* stg = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES + 256) + wq * (32 * 33);
     const uint32_t tempty_leader = CG == 2 ? map_to_rank(smem_u32(&tempty_bar[0]), 0) : smem_u32(&tempty_bar[0]);
     int acc = 0;
     uint32_t acc_ph = 0;
@@ -447,41 +449,78 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
       const TileCoord tc = decode_tile(g, t, BN, CG);
       mbar_wait(smem_u32(&tfull_bar[acc]), acc_ph);
       tc_fence_after();
-      const int64_t m = (int64_t)tc.m0 + (int64_t)rank * BM + wq * 32 + lane;
+      const int64_t m_warp = (int64_t)tc.m0 + (int64_t)rank * BM + wq * 32;  // first row of this warp
+      const int64_t m = m_warp + lane;
       const bool row_ok = m < g.M;
       const bool halo = row_ok && halo_row(g, m);
       const bool raw_out = g.partial != nullptr;
-      float* out_row = raw_out ? g.partial + (int64_t)tc.split * g.split_stride + m * g.ldc : g.c + m * g.ldc;
-      const float* mrow = g.mask ? g.mask + m * g.ldm : nullptr;
+      float* out_base = raw_out ? g.partial + (int64_t)tc.split * g.split_stride : g.c;
+      const float* mrow = (g.mask && row_ok) ? g.mask + m * g.ldm : nullptr;
 #pragma unroll 1
       for (int cb = 0; cb < BN / 32; ++cb) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN + cb * 32, v);
         tmem_ld_wait();
         const int nb = tc.n0 + cb * 32;
-        if (!row_ok || nb >= g.N) continue;
-        float f[32];
+        if (nb >= g.N) continue;  // warp-uniform
+        // 1) per-row epilogue math (thread = row), staged into this warp's smem block
+        const bool full = vec && nb + 32 <= g.N;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float x = __uint_as_float(v[j]);
-          const int n = nb + j;
-          if (!raw_out && n < g.N) {
-            if (g.bias) x += __ldg(g.bias + n);
-            if (g.relu) x = fmaxf(x, 0.f);
-            if (mrow) x = (__ldg(mrow + n) > 0.f) ? x : 0.f;
-            if (halo) x = 0.f;
+        for (int j = 0; j < 32; j += 4) {
+          float x[4] = {__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                        __uint_as_float(v[j + 3])};
+          if (!raw_out) {
+            if (g.bias) {
+              if (full) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + nb + j));
+                x[0] += b4.x; x[1] += b4.y; x[2] += b4.z; x[3] += b4.w;
+              } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                  if (nb + j + i < g.N) x[i] += __ldg(g.bias + nb + j + i);
+              }
+            }
+            if (g.relu) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) x[i] = fmaxf(x[i], 0.f);
+            }
+            if (mrow) {
+              float mk[4];
+              if (full && (g.ldm % 4) == 0) {
+                const float4 m4 = __ldg(reinterpret_cast<const float4*>(mrow + nb + j));
+                mk[0] = m4.x; mk[1] = m4.y; mk[2] = m4.z; mk[3] = m4.w;
+              } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) mk[i] = (nb + j + i < g.N) ? __ldg(mrow + nb + j + i) : 0.f;
+              }
+#pragma unroll
+              for (int i = 0; i < 4; ++i) x[i] = mk[i] > 0.f ? x[i] : 0.f;
+            }
+            if (halo) x[0] = x[1] = x[2] = x[3] = 0.f;
           }
-          f[j] = x;
-        }
-        if (vec && nb + 32 <= g.N) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(out_row + nb + j) = make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (nb + j < g.N) out_row[nb + j] = f[j];
+          for (int i = 0; i < 4; ++i) stg[lane * 33 + j + i] = x[i];
         }
+        __syncwarp();
+        // 2) coalesced stores: each instruction writes 4 rows x 128 contiguous bytes
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int r = it * 4 + (lane >> 3);
+          const int c4 = (lane & 7) * 4;
+          const int64_t row = m_warp + r;
+          if (row < g.M) {
+            float* dst = out_base + row * g.ldc + nb + c4;
+            const float* src = stg + r * 33 + c4;
+            if (full) {
+              *reinterpret_cast<float4*>(dst) = make_float4(src[0], src[1], src[2], src[3]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (nb + c4 + i < g.N) dst[i] = src[i];
+            }
+          }
+        }
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();

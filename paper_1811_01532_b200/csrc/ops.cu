@@ -179,6 +179,36 @@ __global__ void __launch_bounds__(256) im2col_table_kernel(const float* __restri
     toff[kk] = (u * Wxp + v) * xl.ld + c;
   }
   const int Hp = Ho + 2 * P, Wp = Wo + 2 * P;
+  __syncthreads();
+  if (ldcol % 4 == 0) {
+    // flat float4 mapping: 4 consecutive columns of one row per thread (a float4
+    // never straddles rows since ldcol % 4 == 0); row decoded once per float4
+    const int64_t total4 = M * ldcol / 4;
+    const int q4 = (int)(ldcol / 4);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total4; e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t m = e / q4;
+      const int kk0 = (int)(e - m * q4) * 4;
+      const int wo = (int)(m % Wp) - P;
+      const int64_t q = m / Wp;
+      const int ho = (int)(q % Hp) - P;
+      const int b = (int)(q / Hp);
+      float o[4] = {0.f, 0.f, 0.f, 0.f};
+      if (ho >= 0 && ho < Ho && wo >= 0 && wo < Wo) {
+        const int h0 = ho * s - p, w0 = wo * s - p;
+        const int64_t base = (((int64_t)b * (xl.H + 2 * xl.pad) + h0 + xl.pad) * Wxp + w0 + xl.pad) * xl.ld;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int kk = kk0 + i;
+          if (kk < K) {
+            const int hi = h0 + tu[kk], wi = w0 + tv[kk];
+            if (hi >= 0 && hi < xl.H && wi >= 0 && wi < xl.W) o[i] = __ldg(x + base + toff[kk]);
+          }
+        }
+      }
+      reinterpret_cast<float4*>(col)[e] = make_float4(o[0], o[1], o[2], o[3]);
+    }
+    return;
+  }
   for (int64_t r0 = (int64_t)blockIdx.x * IM2COL_ROWS; r0 < M; r0 += (int64_t)gridDim.x * IM2COL_ROWS) {
     __syncthreads();
     if (threadIdx.x < IM2COL_ROWS) {

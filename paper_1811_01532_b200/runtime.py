@@ -154,11 +154,14 @@ class Program:
     """
 
     def __init__(self, graph: Graph, precision: int = 3, device=None, in_place: bool = False,
-                 collective=None, bucket_bytes: int = 64 << 20):
+                 collective=None, bucket_bytes: int = 64 << 20, autotune: bool | None = None):
         import torch
+
+        import os
 
         self._collectives: list = []
         self.bucket_bytes = bucket_bytes
+        self.autotune = autotune if autotune is not None else os.environ.get("WAP_AUTOTUNE", "1") != "0"
         self.buckets: list = []
 
         self.torch = torch
@@ -464,6 +467,7 @@ class Program:
         d.splits = splits
         call = GemmCall(d, device=self.device)
         step = _GemmStep(name, call)
+        step.desc = d
         from .workloads import node_flops
 
         nid = name[:-5] if name.endswith("/dcol") else name
@@ -532,10 +536,46 @@ class Program:
                 self._lower_sgd(n)
             else:
                 raise EvalError(f"no GPU rule for kind {k.value}")
+        if self.autotune:
+            self._autotune_gemms()
         self._schedule_collectives()
         self._fuse_updates()
         self.steps.extend(self.update_steps)
         self.update_steps = []
+
+    def _autotune_gemms(self, reps: int = 3) -> None:
+        """Per-GEMM launch configuration by measurement: one CTA vs a CTA pair
+        (cta_group::2), each with its own split-K choice. Buffers are already
+        allocated; timings are data-independent."""
+        from .kernels import GemmCall
+
+        torch = self.torch
+        stream = torch.cuda.current_stream(self.device)
+        s = N.stream_ptr()
+        for st in self.steps + self.update_steps:
+            if not isinstance(st, _GemmStep) or st.desc.M <= 128:
+                continue
+            best, best_ms = st.call, None
+            for cluster in (1, 2):
+                d = type(st.desc).from_buffer_copy(st.desc)
+                d.cluster = cluster
+                d.workspace, d.workspace_bytes = None, 0
+                try:
+                    call = GemmCall(d, device=self.device)
+                except Exception:
+                    continue
+                N.check(self.L.wap_gemm_plan_run(call._plan, s), "autotune warm-up")
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(reps):
+                    N.check(self.L.wap_gemm_plan_run(call._plan, s), "autotune")
+                e1.record(stream)
+                e1.synchronize()
+                ms = e0.elapsed_time(e1) / reps
+                if best_ms is None or ms < best_ms:
+                    best, best_ms = call, ms
+            st.call = best
+            st.tuned_ms = best_ms
 
     def _schedule_collectives(self) -> None:
         """Bucket the rank-local gradient allreduces and overlap them with backward.
