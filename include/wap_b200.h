@@ -71,6 +71,7 @@ typedef struct {
   int32_t splits;                   /* split-K factor, 0 = automatic */
   int32_t block_n;                  /* 0 = automatic, else 64/128/192/256 */
   int32_t cluster;                  /* 0 = automatic, 1 = one CTA, 2 = CTA pair (cta_group::2) */
+  int32_t window;                   /* 3xTF32 shifted A: 0 = halo-window reuse when it fits, -1 = off */
   float* workspace;                 /* split-K partials, wap_gemm_workspace_bytes() */
   int64_t workspace_bytes;
 } wap_gemm_desc_t;

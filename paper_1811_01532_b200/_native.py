@@ -54,6 +54,7 @@ class wap_gemm_desc_t(C.Structure):
         ("splits", C.c_int32),
         ("block_n", C.c_int32),
         ("cluster", C.c_int32),
+        ("window", C.c_int32),
         ("workspace", C.c_void_p),
         ("workspace_bytes", C.c_int64),
     ]

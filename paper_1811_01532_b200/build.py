@@ -23,7 +23,7 @@ INCLUDE = PKG.parent / "include"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
-         "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"]
+         "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"] + os.environ.get("WAP_NVCC_EXTRA", "").split()
 
 
 def _headers_mtime() -> float:

@@ -108,6 +108,35 @@ Shape plan_shape(const wap_gemm_desc_t& d) {
   return s;
 }
 
+template <int CG>
+int win_smem_cg(int bn, int boxes) {
+  switch (bn) {
+    case 64: return smem_bytes_for<64, 3, CG, true>(boxes);
+    case 128: return smem_bytes_for<128, 3, CG, true>(boxes);
+    case 192: return smem_bytes_for<192, 3, CG, true>(boxes);
+    default: return smem_bytes_for<256, 3, CG, true>(boxes);
+  }
+}
+
+// Halo-window reuse for a 3xTF32 K-major A with filter taps (see gemm_tc.cuh WIN).
+void plan_window(const wap_gemm_desc_t& d, const Shape& s, int& boxes, int& off_min) {
+  boxes = 0;
+  off_min = 0;
+  const wap_operand_t& a = d.a;
+  if (d.precision != 3 || a.mn_major || a.tap_period <= 0 || a.ntaps < 2 || d.window < 0) return;
+  if ((int64_t)a.ntaps * a.tap_period != d.K) return;
+  int mn = a.off[0], mx = a.off[0];
+  for (int t = 1; t < a.ntaps; ++t) {
+    mn = std::min(mn, (int)a.off[t]);
+    mx = std::max(mx, (int)a.off[t]);
+  }
+  const int nb = wap_ceil_div(BM + (mx - mn), BM);
+  const int smem = s.cg == 2 ? win_smem_cg<2>(s.bn, nb) : win_smem_cg<1>(s.bn, nb);
+  if (smem > kMaxDynSmem) return;
+  boxes = nb;
+  off_min = mn;
+}
+
 int validate_operand(const wap_operand_t& op, const char* name) {
   WAP_CHECK_ARG(op.ntaps >= 1 && op.ntaps <= WAP_MAX_TAPS, "%s.ntaps=%d out of [1,%d]", name, op.ntaps,
                 WAP_MAX_TAPS);
@@ -154,6 +183,8 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
   g.halo_pad = d.halo_pad;
   g.halo_h = d.halo_h;
   g.halo_w = d.halo_w;
+  plan_window(d, s, g.win_boxes, g.win_off_min);
+  p->win = g.win_boxes > 0 ? 1 : 0;
   g.partial = nullptr;
   g.split_stride = d.M * d.ldc;
   if (s.splits > 1) {

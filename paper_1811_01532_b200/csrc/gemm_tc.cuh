@@ -32,6 +32,11 @@ constexpr int BM = 128;  // rows per CTA
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row
 constexpr int kSmemBudget = 204 * 1024;  // + 16.5 KB epilogue staging below
 constexpr int kEpiStage = 4 * 32 * 33 * 4;
+constexpr int kBarBytes = 512;  // mbarriers + TMEM address holder
+#ifndef WAP_SPLIT_GROUPS
+#define WAP_SPLIT_GROUPS 2
+#endif
+constexpr int kSplitGroups = WAP_SPLIT_GROUPS;  // 3xTF32 splitter groups (8 warps each)
 
 struct OperandDev {
   int32_t mn_major, tap_period, ntaps;
@@ -52,6 +57,7 @@ struct GemmArgs {
   const float* mask;
   int64_t ldm;
   int32_t halo_pad, halo_h, halo_w;
+  int32_t win_boxes, win_off_min;  // WIN: 128-row TMA boxes per A halo window, min tap shift
 };
 
 // 3xTF32 keeps the A operand in TMEM (tcgen05 "TS" form): the splitter warps
@@ -61,23 +67,30 @@ struct GemmArgs {
 //   [0, ACC_BUFS*BN)                accumulators
 //   [A_COL0 + s*64, +32)            A big  of stage s   (lane = row, column = k)
 //   [A_COL0 + s*64 + 32, +32)       A small of stage s
-template <int BN, int PREC, int CG>
+// WIN (3xTF32, K-major A with filter taps): A is not staged per k-step. For each
+// 32-channel chunk the producer loads ONE halo window of A rows
+// [m0 + min_tap_shift, m0 + 128 + max_tap_shift) and the splitter cuts every
+// tap's 128-row A tile out of it (tap-inner k order), so a k x k conv reads its
+// activations once per chunk instead of k^2 times.
+template <int BN, int PREC, int CG, bool WIN = false>
 struct Cfg {
   static constexpr int B_ROWS = BN / CG;  // B rows staged by each CTA
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = B_ROWS * BK * 4;
-  // PREC 3 smem stage: A raw | B raw | B small
-  static constexpr int STAGE_BYTES = PREC == 3 ? (A_BYTES + 2 * B_BYTES) : (A_BYTES + B_BYTES);
+  static constexpr int A_OFF = WIN ? 0 : A_BYTES;  // B offset inside a stage
+  // PREC 3 smem stage: [A raw] | B raw | B small
+  static constexpr int STAGE_BYTES = PREC == 3 ? (A_OFF + 2 * B_BYTES) : (A_BYTES + B_BYTES);
   // two accumulators (epilogue overlap) only if >= 4 A stages still fit in TMEM
   static constexpr int ACC_BUFS = (PREC == 3 && 512 - 2 * BN < 4 * 64) ? 1 : 2;
   static constexpr int A_COL0 = ACC_BUFS * BN;
   static constexpr int TMEM_A_SLOTS = PREC == 3 ? (512 - A_COL0) / 64 : 64;
   static constexpr int STAGES_SMEM = kSmemBudget / STAGE_BYTES;
-  static constexpr int STAGES_A = STAGES_SMEM < TMEM_A_SLOTS ? STAGES_SMEM : TMEM_A_SLOTS;
-  static constexpr int STAGES = STAGES_A > 8 ? 8 : STAGES_A;
+  // smem stages (TMA prefetch depth) and TMEM A slots (split -> MMA) are separate rings
+  static constexpr int A_SLOTS = PREC == 3 ? (TMEM_A_SLOTS > 8 ? 8 : TMEM_A_SLOTS) : 1;
+  static constexpr int STAGES = WIN ? 6 : (STAGES_SMEM > 8 ? 8 : STAGES_SMEM);
   static constexpr int TMEM_COLS = PREC == 3 ? 512 : ((2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512));
-  static constexpr int THREADS = PREC == 3 ? 512 : 256;  // + 2 x 4 splitter warps
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + kEpiStage;
+  static constexpr int THREADS = PREC == 3 ? 256 + 256 * kSplitGroups : 256;  // + splitter warp groups
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + kBarBytes + kEpiStage;
   static_assert(STAGES >= 2, "need at least two pipeline stages");
   static_assert(B_ROWS % 32 == 0, "B rows per CTA must be a multiple of 32");
 };
@@ -114,6 +127,40 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
       "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
       "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
       "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+// k-columns [16*half, 16*half+16) of A row m, K-major SWIZZLE_128B tile
+__device__ __forceinline__ void load_a_half_kmajor(const uint8_t* tile, int m, int half, uint32_t (&v)[16]) {
+  const uint8_t* row = tile + m * 128;
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    const int j = half * 4 + jj;
+    const uint4 q = *reinterpret_cast<const uint4*>(row + ((j ^ (m & 7)) << 4));
+    v[4 * jj] = q.x;
+    v[4 * jj + 1] = q.y;
+    v[4 * jj + 2] = q.z;
+    v[4 * jj + 3] = q.w;
+  }
+}
+
+// k-rows [16*half, 16*half+16) of A column m, MN-major 32B-atom tile
+__device__ __forceinline__ void load_a_half_mnmajor(const uint8_t* tile, int m, int half, uint32_t (&v)[16]) {
+  const uint8_t* blk = tile + (m >> 5) * (BK * 128);
+  const int mi = m & 31;
+#pragma unroll
+  for (int kk = 0; kk < 16; ++kk) {
+    const int k = half * 16 + kk;
+    v[kk] = *reinterpret_cast<const uint32_t*>(blk + k * 128 + ((((mi >> 3) ^ (k & 3))) << 5) + (mi & 7) * 4);
+  }
+}
+
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
 }
 
@@ -256,6 +303,16 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
@@ -304,6 +361,32 @@ __device__ __forceinline__ void umma_commit_cg(uint32_t bar) {
   }
 }
 
+
+// Optional role/wait tracing (build with -DWAP_GEMM_TRACE): block 0 records, per
+// role, total cycles and cycles spent in each barrier wait (slots 1..3).
+#ifdef WAP_GEMM_TRACE
+__device__ unsigned long long g_gemm_trace[64];
+#define TRACE_BEGIN() unsigned long long _tr[4] = {0, 0, 0, 0}; const unsigned long long _t0 = clock64()
+#define TW(slot, expr) do { const unsigned long long _a = clock64(); expr; _tr[slot] += clock64() - _a; } while (0)
+#define TRACE_END()                                                                           \
+  do {                                                                                        \
+    int _role = -1;                                                                           \
+    if (warp == 0 && lane == 0) _role = 0;                                                    \
+    else if (warp == 1 && lane == 0) _role = 1;                                               \
+    else if (warp == 4 && lane == 0) _role = 2;                                               \
+    else if (warp == 8 && lane == 0) _role = 3;                                               \
+    else if (warp == 16 && lane == 0) _role = 4;                                              \
+    if (blockIdx.x == 0 && _role >= 0) {                                                      \
+      g_gemm_trace[_role * 4] = clock64() - _t0;                                              \
+      for (int _i = 1; _i < 4; ++_i) g_gemm_trace[_role * 4 + _i] = _tr[_i];                  \
+    }                                                                                         \
+  } while (0)
+#else
+#define TRACE_BEGIN() do {} while (0)
+#define TW(slot, expr) expr
+#define TRACE_END() do {} while (0)
+#endif
+
 struct TileCoord {
   int m0, n0, split, kc_begin, kc_end;
 };
@@ -321,15 +404,20 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& g, int t, int B
   return c;
 }
 
-template <int BN, bool A_MN, bool B_MN, int PREC, int CG>
-__global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
+template <int BN, bool A_MN, bool B_MN, int PREC, int CG, bool WIN = false>
+__global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ GemmArgs g) {
-  using C = Cfg<BN, PREC, CG>;
+  using C = Cfg<BN, PREC, CG, WIN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint8_t* win_base = smem + STAGES * C::STAGE_BYTES;                  // 2 A halo windows (WIN)
+  const int win_bytes = WIN ? g.win_boxes * C::A_BYTES : 0;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(win_base + 2 * win_bytes);
+  uint64_t* wfull_bar = bars + 3 * STAGES + 5;   // [2] window landed (WIN)
+  uint64_t* wempty_bar = bars + 3 * STAGES + 7;  // [2] window consumed by both splitter groups (WIN)
+  uint64_t* aslot_bar = bars + 3 * STAGES + 9;   // [A_SLOTS] TMEM A slot free again (MMA commit)
   uint64_t* full_bar = bars;                    // TMA landed (leader-side for CG=2 & TF32)
   uint64_t* empty_bar = bars + STAGES;          // smem slot free (MMA commit, multicast)
   uint64_t* conv_bar = bars + 2 * STAGES;       // 3xTF32 split done (leader-side)
@@ -346,8 +434,18 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
   const int n_tiles_total = g.m_tiles * g.n_tiles * g.splits;
 
   auto stage_a = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES); };
-  auto stage_b = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES + C::A_BYTES); };
-  auto stage_bs = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES + C::A_BYTES + C::B_BYTES); };
+  auto stage_b = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES + C::A_OFF); };
+  auto stage_bs = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES + C::A_OFF + C::B_BYTES); };
+  // WIN: k-chunk kc -> (channel chunk, tap), tap innermost; returns the flat k
+  const int ntaps = WIN ? g.a.ntaps : 1;
+  auto k_of = [&](int kc) {
+    if constexpr (WIN) {
+      const int cidx = kc / ntaps, tap = kc - cidx * ntaps;
+      return tap * g.a.tap_period + cidx * BK;
+    } else {
+      return kc * BK;
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -355,11 +453,16 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(&full_bar[s]), 1);
       mbar_init(smem_u32(&empty_bar[s]), 1);
-      mbar_init(smem_u32(&conv_bar[s]), 4 * CG);  // one arrive per splitter warp
+      mbar_init(smem_u32(&conv_bar[s]), CG);  // one arrive per CTA of the pair
     }
+    for (int j = 0; j < C::A_SLOTS; ++j) mbar_init(smem_u32(&aslot_bar[j]), 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&tfull_bar[i]), 1);
-      mbar_init(smem_u32(&tempty_bar[i]), 4 * CG);  // one arrive per epilogue warp
+      mbar_init(smem_u32(&tempty_bar[i]), CG);  // one arrive per CTA of the pair
+      if (WIN) {
+        mbar_init(smem_u32(&wfull_bar[i]), 1);
+        mbar_init(smem_u32(&wempty_bar[i]), kSplitGroups);  // every splitter group
+      }
     }
     mbar_fence_init();
   }
@@ -372,18 +475,39 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
   if constexpr (CG == 2) cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  TRACE_BEGIN();
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs) ----------------
       int s = 0;
       uint32_t ph = 0;
+      int wc = 0;  // windows issued
       for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
         const TileCoord tc = decode_tile(g, t, BN, CG);
         const int a_row0 = tc.m0 + (int)rank * BM;
         const int b_row0 = tc.n0 + (int)rank * C::B_ROWS;
         for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc) {
-          mbar_wait(smem_u32(&empty_bar[s]), ph ^ 1);
+          if constexpr (WIN) {
+            const int cidx = kc / ntaps, tap = kc - cidx * ntaps;
+            if (tap == 0 || kc == tc.kc_begin) {
+              const int ws = wc & 1;
+              TW(1, mbar_wait(smem_u32(&wempty_bar[ws]), ((wc >> 1) & 1) ^ 1));
+              const uint32_t wb = smem_u32(&wfull_bar[ws]);
+              mbar_arrive_expect_tx(wb, win_bytes);
+              for (int bx = 0; bx < g.win_boxes; ++bx)
+                tma_load_2d(smem_u32(win_base + ws * win_bytes + bx * C::A_BYTES), &tmA, wb, cidx * BK,
+                            a_row0 + g.win_off_min + bx * BM);
+              ++wc;
+            }
+            TW(2, mbar_wait(smem_u32(&empty_bar[s]), ph ^ 1));
+            const uint32_t fb = smem_u32(&full_bar[s]);
+            mbar_arrive_expect_tx(fb, C::B_BYTES);
+            load_operand<C::B_ROWS, B_MN, 1>(&tmB, g.b, stage_b(s), fb, b_row0, k_of(kc));
+            if (++s == STAGES) { s = 0; ph ^= 1; }
+            continue;
+          }
+          TW(2, mbar_wait(smem_u32(&empty_bar[s]), ph ^ 1));
           uint32_t fb = smem_u32(&full_bar[s]);
           if constexpr (CG == 2 && PREC == 1) {
             fb &= 0xFEFFFFFFu;  // the leader's barrier collects both CTAs' bytes
@@ -400,54 +524,82 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    if (leader) {
       // ---------------- MMA issuer (leader CTA) ----------------
+      // The whole warp runs the loop (so descriptor math stays warp-uniform and
+      // lives in uniform registers); one elected lane issues the tcgen05 ops.
       // A lives in TMEM (K-major by construction) for 3xTF32
       constexpr uint32_t idesc = make_idesc_tf32(BM * CG, BN, PREC == 3 ? false : A_MN, B_MN);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
       uint32_t acc_ph = 0;
+      int aj = 0;  // TMEM A slot of the current step
       for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
         const TileCoord tc = decode_tile(g, t, BN, CG);
-        mbar_wait(smem_u32(&tempty_bar[acc]), acc_ph ^ 1);
+        TW(1, mbar_wait(smem_u32(&tempty_bar[acc]), acc_ph ^ 1));
         tc_fence_after();
         const uint32_t dacc = tmem_base + acc * BN;
         for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc) {
-          if constexpr (PREC == 3) mbar_wait(smem_u32(&conv_bar[s]), ph);
-          else mbar_wait(smem_u32(&full_bar[s]), ph);
+          if constexpr (PREC == 3) TW(2, mbar_wait(smem_u32(&conv_bar[s]), ph));
+          else TW(2, mbar_wait(smem_u32(&full_bar[s]), ph));
           tc_fence_after();
+          // descriptors built once per stage; the k-steps only advance the
+          // 14-bit start-address field (addr >> 4), keeping the issue loop short
+          constexpr uint64_t kB = B_MN ? (1024 >> 4) : (32 >> 4);
+          constexpr uint64_t kA = A_MN ? (1024 >> 4) : (32 >> 4);
+          const uint64_t bd0 = operand_desc<B_MN>(stage_b(s), 0);
+          const uint64_t bsd0 = operand_desc<B_MN>(stage_bs(s), 0);
+          const uint64_t ad0 = operand_desc<A_MN>(stage_a(s), 0);
+          const uint32_t a_big0 = tmem_base + C::A_COL0 + aj * 64;
+          const uint32_t first0 = kc > tc.kc_begin ? 1u : 0u;
+#ifdef WAP_GEMM_TMA_ONLY
+          // diagnostic: measure the TMA stream alone (no MMA)
+          if (elect_one()) mbar_arrive(smem_u32(&empty_bar[s]));
+          if (false) {
+#else
+          if (elect_one()) {
+#endif
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint64_t bd = operand_desc<B_MN>(stage_b(s), kk);
-            const uint32_t first = (kc > tc.kc_begin || kk > 0) ? 1u : 0u;
-            if constexpr (PREC == 3) {
-              const uint32_t a_big = tmem_base + C::A_COL0 + s * 64 + kk * 8;
-              umma_ts_cg<CG>(dacc, a_big + 32, bd, idesc, first);                          // small * B
-              umma_ts_cg<CG>(dacc, a_big, operand_desc<B_MN>(stage_bs(s), kk), idesc, 1u);  // A * small
-              umma_ts_cg<CG>(dacc, a_big, bd, idesc, 1u);                                   // big * big
-            } else {
-              umma_cg<CG>(dacc, operand_desc<A_MN>(stage_a(s), kk), bd, idesc, first);
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint64_t bd = bd0 + kk * kB;
+              const uint32_t first = kk > 0 ? 1u : first0;
+              if constexpr (PREC == 3) {
+                const uint32_t a_big = a_big0 + kk * 8;
+                umma_ts_cg<CG>(dacc, a_big + 32, bd, idesc, first);        // small * B
+                umma_ts_cg<CG>(dacc, a_big, bsd0 + kk * kB, idesc, 1u);    // A * small
+                umma_ts_cg<CG>(dacc, a_big, bd, idesc, 1u);                // big * big
+              } else {
+                umma_cg<CG>(dacc, ad0 + kk * kA, bd, idesc, first);
+              }
             }
+            umma_commit_cg<CG>(smem_u32(&empty_bar[s]));
+            if constexpr (PREC == 3) umma_commit_cg<CG>(smem_u32(&aslot_bar[aj]));
           }
-          umma_commit_cg<CG>(smem_u32(&empty_bar[s]));
+          __syncwarp();
           if (++s == STAGES) { s = 0; ph ^= 1; }
+          if (++aj == C::A_SLOTS) aj = 0;
         }
-        umma_commit_cg<CG>(smem_u32(&tfull_bar[acc]));
+#ifdef WAP_GEMM_TMA_ONLY
+        if (elect_one()) mbar_arrive(smem_u32(&tfull_bar[acc]));
+#else
+        if (elect_one()) umma_commit_cg<CG>(smem_u32(&tfull_bar[acc]));
+#endif
+        __syncwarp();
         if (++acc == C::ACC_BUFS) { acc = 0; acc_ph ^= 1; }
       }
     }
   } else if (warp >= 4 && warp < 8) {
     // ---------------- epilogue ----------------
     const int wq = warp - 4;  // TMEM lane quarter
-    float* stg = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES + 256) + wq * (32 * 33);
+    float* stg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes) + wq * (32 * 33);
     const uint32_t tempty_leader = CG == 2 ? map_to_rank(smem_u32(&tempty_bar[0]), 0) : smem_u32(&tempty_bar[0]);
     int acc = 0;
     uint32_t acc_ph = 0;
     const bool vec = (g.ldc % 4) == 0;
     for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
       const TileCoord tc = decode_tile(g, t, BN, CG);
-      mbar_wait(smem_u32(&tfull_bar[acc]), acc_ph);
+      TW(1, mbar_wait(smem_u32(&tfull_bar[acc]), acc_ph));
       tc_fence_after();
       const int64_t m_warp = (int64_t)tc.m0 + (int64_t)rank * BM + wq * 32;  // first row of this warp
       const int64_t m = m_warp + lane;
@@ -523,59 +675,97 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG>::THREADS, 1)
         __syncwarp();
       }
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
+      named_bar_sync(1, 128);
+      if (wq == 0 && lane == 0) {
+        if (CG == 2 && !leader) mbar_arrive_cluster(tempty_leader + acc * 8);
         else mbar_arrive(smem_u32(&tempty_bar[acc]));
       }
       if (++acc == C::ACC_BUFS) { acc = 0; acc_ph ^= 1; }
     }
   } else if (PREC == 3 && warp >= 8) {
     // ---------------- 3xTF32 operand split (both CTAs) ----------------
-    // Two groups of 4 warps alternate stages (two stages in flight). Within a
-    // group, thread ct owns row ct of the CTA's A tile = TMEM lane ct.
-    const int group = (warp - 8) >> 2;
-    const int ct = (threadIdx.x - 256) & 127;
+    // kSplitGroups groups of 8 warps alternate stages. Within a group, warp
+    // (q, half) owns TMEM lane quarter q = warp % 4 (the tcgen05 lane-access
+    // rule) and k-columns [16*half, 16*half + 16); thread row ct = 32q + lane.
+    const int sw = warp - 8;
+    const int group = sw >> 3;  // 0 .. kSplitGroups-1
+    const int half = (sw >> 2) & 1;
+    const int ct = (warp & 3) * 32 + lane;
+    const int gt = (sw & 7) * 32 + lane;  // thread index inside the group (0..255)
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t conv_leader = CG == 2 ? map_to_rank(smem_u32(&conv_bar[0]), 0) : smem_u32(&conv_bar[0]);
     int s = 0;
     uint32_t ph = 0;
     int it = 0;
+    int wc = 0, wslot = 0;       // WIN: windows seen, current slot
+    bool wwaited = false;        // WIN: this group has waited for the current window
     for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
       const TileCoord tc = decode_tile(g, t, BN, CG);
       for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc, ++it) {
-        if ((it & 1) != group) {
+        int tap = 0;
+        bool last_in_win = false;
+        if constexpr (WIN) {
+          const int cidx = kc / ntaps;
+          tap = kc - cidx * ntaps;
+          if (tap == 0 || kc == tc.kc_begin) {
+            wslot = wc & 1;
+            ++wc;
+            wwaited = false;
+          }
+          last_in_win = (tap == ntaps - 1) || (kc == tc.kc_end - 1);
+        }
+        if ((it % kSplitGroups) != group) {
+          // this group's own steps of the window are done (each ended in a named barrier)
+          if (WIN && last_in_win && gt == 0) mbar_arrive(smem_u32(&wempty_bar[wslot]));
           if (++s == STAGES) { s = 0; ph ^= 1; }
           continue;
         }
-        mbar_wait(smem_u32(&full_bar[s]), ph);
+        TW(1, mbar_wait(smem_u32(&full_bar[s]), ph));
         uint8_t* base = smem + s * C::STAGE_BYTES;
-        uint32_t v[32], w[32];
-        if constexpr (A_MN) load_a_row_mnmajor(base, ct, v);
-        else load_a_row_kmajor(base, ct, v);
+        uint32_t v[16], w[16];
+        if constexpr (WIN) {
+          if (!wwaited) {
+            TW(2, mbar_wait(smem_u32(&wfull_bar[wslot]), ((wc - 1) >> 1) & 1));
+            wwaited = true;
+          }
+          // row ct of this tap's tile = window row ct + shift(tap) - min shift
+          load_a_half_kmajor(win_base + wslot * win_bytes, ct + g.a.off[tap] - g.win_off_min, half, v);
+        } else if constexpr (A_MN) {
+          load_a_half_mnmajor(base, ct, half, v);
+        } else {
+          load_a_half_kmajor(base, ct, half, v);
+        }
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < 16; ++j) {
           const uint32_t big = v[j] & 0xFFFFE000u;
           w[j] = __float_as_uint(__uint_as_float(v[j]) - __uint_as_float(big));
           v[j] = big;
         }
-        const uint32_t acol = tmem_base + lane_base + C::A_COL0 + s * 64;
-        tmem_st_32x32b_x32(acol, v);
-        tmem_st_32x32b_x32(acol + 32, w);
-        split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_BYTES),
-                         reinterpret_cast<uint32_t*>(base + C::A_BYTES + C::B_BYTES), C::B_ROWS * BK, ct, 128);
+        // TMEM A slot of this step: free once the MMAs of its previous use committed
+        const int aj = it % C::A_SLOTS;
+        mbar_wait(smem_u32(&aslot_bar[aj]), ((it / C::A_SLOTS) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t acol = tmem_base + lane_base + C::A_COL0 + aj * 64 + half * 16;
+        tmem_st_32x32b_x16(acol, v);
+        tmem_st_32x32b_x16(acol + 32, w);
+        split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_OFF),
+                         reinterpret_cast<uint32_t*>(base + C::A_OFF + C::B_BYTES), C::B_ROWS * BK, gt, 256);
         tmem_st_wait();
         tc_fence_before();
         fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          if constexpr (CG == 2) mbar_arrive_cluster(conv_leader + s * 8);
+        // one arrival per CTA: group-local named barrier, then a single thread
+        // signals (CTA-scope in the leader, cluster-scope release from the peer)
+        TW(3, named_bar_sync(2 + group, 256));
+        if (gt == 0) {
+          if (CG == 2 && !leader) mbar_arrive_cluster(conv_leader + s * 8);
           else mbar_arrive(smem_u32(&conv_bar[s]));
+          if (WIN && last_in_win) mbar_arrive(smem_u32(&wempty_bar[wslot]));
         }
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }
   }
+  TRACE_END();
   tc_fence_before();
   __syncthreads();
   if constexpr (CG == 2) cluster_sync();
@@ -589,22 +779,35 @@ struct Plan {
   CUtensorMap tmA, tmB;
   GemmArgs args;
   int grid;
-  int bn, a_mn, b_mn, prec, cg, splits;
+  int bn, a_mn, b_mn, prec, cg, splits, win;
 };
 
-template <int BN, bool AMN, bool BMN, int PREC, int CG>
+constexpr int kMaxDynSmem = 227 * 1024;
+
+// dynamic shared memory of one launch (WIN adds the two A halo windows)
+template <int BN, int PREC, int CG, bool WIN>
+constexpr int smem_bytes_for(int win_boxes) {
+  return Cfg<BN, PREC, CG, WIN>::SMEM + (WIN ? 2 * win_boxes * Cfg<BN, PREC, CG, WIN>::A_BYTES : 0);
+}
+
+template <int BN, bool AMN, bool BMN, int PREC, int CG, bool WIN = false>
 int launch(const Plan& p, cudaStream_t st) {
-  using C = Cfg<BN, PREC, CG>;
-  auto kern = gemm_tc_kernel<BN, AMN, BMN, PREC, CG>;
+  using C = Cfg<BN, PREC, CG, WIN>;
+  auto kern = gemm_tc_kernel<BN, AMN, BMN, PREC, CG, WIN>;
   static bool attr_set = false;
   if (!attr_set) {
-    WAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    WAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     attr_set = true;
+  }
+  const int smem = smem_bytes_for<BN, PREC, CG, WIN>(p.args.win_boxes);
+  if (smem > kMaxDynSmem) {
+    wap_set_error("GEMM shared memory %d exceeds %d (window of %d boxes)", smem, kMaxDynSmem, p.args.win_boxes);
+    return WAP_ENOTSUP;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.grid);
   cfg.blockDim = dim3(C::THREADS);
-  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   int na = 0;
@@ -624,6 +827,12 @@ int launch(const Plan& p, cudaStream_t st) {
 // dispatch over the three major combinations used on the WAP path
 template <int BN, int PREC, int CG>
 int launch_majors(const Plan& p, cudaStream_t st) {
+  if constexpr (PREC == 3) {
+    if (p.win && !p.a_mn) {
+      if (p.b_mn) return launch<BN, false, true, PREC, CG, true>(p, st);
+      return launch<BN, false, false, PREC, CG, true>(p, st);
+    }
+  }
   if (!p.a_mn && p.b_mn) return launch<BN, false, true, PREC, CG>(p, st);
   if (!p.a_mn && !p.b_mn) return launch<BN, false, false, PREC, CG>(p, st);
   if (p.a_mn && p.b_mn) return launch<BN, true, true, PREC, CG>(p, st);

@@ -13,3 +13,11 @@ static int by_bn(const Plan& p, cudaStream_t st) {
 }
 int launch_prec3(const Plan& p, cudaStream_t st) { return p.cg == 2 ? by_bn<2>(p, st) : by_bn<1>(p, st); }
 }  // namespace wapgemm
+
+#ifdef WAP_GEMM_TRACE
+// Diagnostic builds only: copy block 0's role/wait trace (5 roles x 4 slots).
+extern "C" int wap_gemm_trace_read(unsigned long long* host, int n) {
+  if (n > 64) n = 64;
+  return (int)cudaMemcpyFromSymbol(host, wapgemm::g_gemm_trace, n * sizeof(unsigned long long));
+}
+#endif

@@ -556,9 +556,12 @@ class Program:
             if not isinstance(st, _GemmStep) or st.desc.M <= 128:
                 continue
             best, best_ms = st.call, None
-            for cluster in (1, 2):
+            a = st.desc.a
+            windows = (0, -1) if (self.precision == 3 and not a.mn_major and a.ntaps > 1) else (0,)
+            for cluster, window in [(c, w) for c in (1, 2) for w in windows]:
                 d = type(st.desc).from_buffer_copy(st.desc)
                 d.cluster = cluster
+                d.window = window
                 d.workspace, d.workspace_bytes = None, 0
                 try:
                     call = GemmCall(d, device=self.device)

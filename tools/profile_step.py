@@ -36,10 +36,16 @@ def main():
     names = args.only.split(",")
     sel = [s for s in tr.prog.steps if s.name in names] or [s for s in tr.prog.steps if args.only in s.name]
     print("selected:", [s.name for s in sel], flush=True)
-    for _ in range(args.reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i in range(args.reps):
+        if i == 1:
+            e0.record()
         for s in sel:
             s(N.stream_ptr())
+    e1.record()
     torch.cuda.synchronize()
+    if args.reps > 1:
+        print(f"avg ms per rep: {e0.elapsed_time(e1) / (args.reps - 1):.4f}", flush=True)
 
 
 if __name__ == "__main__":
