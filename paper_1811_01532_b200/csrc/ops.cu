@@ -85,25 +85,56 @@ __global__ void add_n_kernel_packed(PtrPack xs, int n, float* __restrict__ y, in
 // ---------------------------------------------------------------------------
 // GradBias: column sums, pass 1 = per-chunk partials, pass 2 = ordered sum
 // ---------------------------------------------------------------------------
-__global__ void bias_grad_partial(const float* __restrict__ dy, int64_t rows, int ld, int C, int64_t rows_per_chunk,
-                                  float* __restrict__ part) {
-  __shared__ float red[8][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + tx;
+// Block = CW float4 column groups (tx) x RL row lanes (ty), CW*RL = 256. Each
+// thread streams its rows with four independent float4 loads in flight; the
+// row lanes are reduced in a fixed order through shared memory.
+__global__ void __launch_bounds__(256) bias_grad_partial(const float* __restrict__ dy, int64_t rows, int ld, int C,
+                                                         int64_t rows_per_chunk, int CW, float* __restrict__ part) {
+  __shared__ float4 red[256];
+  const int RL = 256 / CW;
+  const int tx = threadIdx.x % CW, ty = threadIdx.x / CW;
+  const int c = (blockIdx.x * CW + tx) * 4;
   const int chunk = blockIdx.y;
   const int64_t r0 = chunk * rows_per_chunk;
   const int64_t r1 = min(rows, r0 + rows_per_chunk);
-  float s = 0.f;
-  if (c < C)
-    for (int64_t r = r0 + ty; r < r1; r += 8) s += dy[r * ld + c];
-  red[ty][tx] = s;
-  __syncthreads();
-  if (ty == 0) {
-    float t = red[0][tx];
-#pragma unroll
-    for (int k = 1; k < 8; ++k) t += red[k][tx];
-    if (c < C) part[(int64_t)chunk * ld + c] = t;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (c < ld) {
+    const float* base = dy + c;
+    int64_t r = r0 + ty;
+    for (; r + 3 * RL < r1; r += 4 * RL) {
+      const float4 a = *reinterpret_cast<const float4*>(base + r * ld);
+      const float4 b = *reinterpret_cast<const float4*>(base + (r + RL) * ld);
+      const float4 e = *reinterpret_cast<const float4*>(base + (r + 2 * RL) * ld);
+      const float4 f = *reinterpret_cast<const float4*>(base + (r + 3 * RL) * ld);
+      s.x += (a.x + b.x) + (e.x + f.x);
+      s.y += (a.y + b.y) + (e.y + f.y);
+      s.z += (a.z + b.z) + (e.z + f.z);
+      s.w += (a.w + b.w) + (e.w + f.w);
+    }
+    for (; r < r1; r += RL) {
+      const float4 a = *reinterpret_cast<const float4*>(base + r * ld);
+      s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
+    }
   }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (ty == 0 && c < C) {
+    float4 t = red[tx];
+    for (int k = 1; k < RL; ++k) {
+      const float4 u = red[k * CW + tx];
+      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+    }
+    float* o = part + (int64_t)chunk * ld + c;
+    o[0] = t.x;
+    if (c + 1 < C) o[1] = t.y;
+    if (c + 2 < C) o[2] = t.z;
+    if (c + 3 < C) o[3] = t.w;
+  }
+}
+
+int bias_cw(const wap_layout_t& l) {
+  const int cols4 = l.ld / 4;
+  return cols4 >= 32 ? 32 : (cols4 >= 16 ? 16 : (cols4 >= 8 ? 8 : (cols4 >= 4 ? 4 : (cols4 >= 2 ? 2 : 1))));
 }
 
 __global__ void bias_grad_final(const float* __restrict__ part, int chunks, int ld, int C, float* __restrict__ db) {
@@ -116,7 +147,8 @@ __global__ void bias_grad_final(const float* __restrict__ part, int chunks, int 
 
 int bias_chunks(const wap_layout_t& l) {
   const int64_t rows = (int64_t)l.B * (l.H + 2 * l.pad) * (l.W + 2 * l.pad);
-  const int ctiles = (l.C + 31) / 32;
+  const int cw = bias_cw(l);
+  const int ctiles = (l.ld / 4 + cw - 1) / cw;
   int64_t chunks = (2 * WAP_NUM_SMS + ctiles - 1) / ctiles;
   const int64_t max_chunks = (rows + 63) / 64;
   if (chunks > max_chunks) chunks = max_chunks;
@@ -550,6 +582,93 @@ __global__ void __launch_bounds__(256) lrn_fast_kernel(const float* __restrict__
   }
 }
 
+// Register-only LRN (size 5): 16 lanes per pixel, VPL float4 (4*VPL channels)
+// per lane, the +-2 channel window crosses lanes through 16-wide shuffles.
+// One coalesced read of x (+dy, mask) and one write per element: HBM-bound.
+template <int VPL, bool BWD>
+__global__ void __launch_bounds__(256) lrn_warp_kernel(const float* __restrict__ x, wap_layout_t xl,
+                                                       const float* __restrict__ dy, wap_layout_t dyl, float alpha,
+                                                       float beta, float k, float* __restrict__ out, wap_layout_t ol,
+                                                       const float* __restrict__ mask, wap_layout_t ml) {
+  constexpr int NV = 4 * VPL;
+  const int lane = threadIdx.x & 31;
+  const int sl = lane & 15;
+  const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int c0 = sl * NV;
+  for (int64_t pbase = wid * 2; pbase < npix; pbase += nw * 2) {
+    const int64_t p = pbase + (lane >> 4);
+    const bool ok = p < npix;
+    int b = 0, h = 0, w = 0;
+    if (ok) pixel_of(xl, p, b, h, w);
+    float v[NV], d[NV], q[NV];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), g = a;
+      if (ok) {
+        a = *reinterpret_cast<const float4*>(x + lidx(xl, b, h, w, c0 + 4 * i));
+        if (BWD) g = *reinterpret_cast<const float4*>(dy + lidx(dyl, b, h, w, c0 + 4 * i));
+      }
+      v[4 * i] = a.x; v[4 * i + 1] = a.y; v[4 * i + 2] = a.z; v[4 * i + 3] = a.w;
+      d[4 * i] = g.x; d[4 * i + 1] = g.y; d[4 * i + 2] = g.z; d[4 * i + 3] = g.w;
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) q[j] = v[j] * v[j];
+    // window sums of squares over channels c-2..c+2
+    float pm2 = __shfl_up_sync(0xffffffffu, q[NV - 2], 1, 16), pm1 = __shfl_up_sync(0xffffffffu, q[NV - 1], 1, 16);
+    float np0 = __shfl_down_sync(0xffffffffu, q[0], 1, 16), np1 = __shfl_down_sync(0xffffffffu, q[1], 1, 16);
+    if (sl == 0) pm2 = pm1 = 0.f;
+    if (sl == 15) np0 = np1 = 0.f;
+    float s[NV], pw[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      float acc = q[j];
+      acc += (j >= 1) ? q[j - 1] : pm1;
+      acc += (j >= 2) ? q[j - 2] : (j == 1 ? pm1 : pm2);
+      acc += (j + 1 < NV) ? q[j + 1] : np0;
+      acc += (j + 2 < NV) ? q[j + 2] : (j + 1 < NV ? np0 : np1);
+      s[j] = k + alpha * acc;
+      pw[j] = exp2f(-beta * __log2f(s[j]));
+    }
+    float o[NV];
+    if (!BWD) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) o[j] = v[j] * pw[j];
+    } else {
+      float t[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) t[j] = d[j] * v[j] * pw[j] / s[j];
+      float tm2 = __shfl_up_sync(0xffffffffu, t[NV - 2], 1, 16), tm1 = __shfl_up_sync(0xffffffffu, t[NV - 1], 1, 16);
+      float tp0 = __shfl_down_sync(0xffffffffu, t[0], 1, 16), tp1 = __shfl_down_sync(0xffffffffu, t[1], 1, 16);
+      if (sl == 0) tm2 = tm1 = 0.f;
+      if (sl == 15) tp0 = tp1 = 0.f;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        float acc = t[j];
+        acc += (j >= 1) ? t[j - 1] : tm1;
+        acc += (j >= 2) ? t[j - 2] : (j == 1 ? tm1 : tm2);
+        acc += (j + 1 < NV) ? t[j + 1] : tp0;
+        acc += (j + 2 < NV) ? t[j + 2] : (j + 1 < NV ? tp0 : tp1);
+        o[j] = d[j] * pw[j] - 2.f * alpha * beta * v[j] * acc;
+      }
+    }
+    if (!ok) continue;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      float4 r = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+      if (BWD && mask) {
+        const float4 m = *reinterpret_cast<const float4*>(mask + lidx(ml, b, h, w, c0 + 4 * i));
+        if (!(m.x > 0.f)) r.x = 0.f;
+        if (!(m.y > 0.f)) r.y = 0.f;
+        if (!(m.z > 0.f)) r.z = 0.f;
+        if (!(m.w > 0.f)) r.w = 0.f;
+      }
+      *reinterpret_cast<float4*>(out + lidx(ol, b, h, w, c0 + 4 * i)) = r;
+    }
+  }
+}
+
 template <bool BWD>
 bool launch_lrn_fast(const float* x, wap_layout_t xl, const float* dy, wap_layout_t dyl, int size, float alpha,
                      float beta, float bias, float* out, wap_layout_t ol, const float* mask, wap_layout_t ml,
@@ -557,6 +676,16 @@ bool launch_lrn_fast(const float* x, wap_layout_t xl, const float* dy, wap_layou
   const bool compact = xl.ld == xl.C && ol.ld == xl.C && (!BWD || dyl.ld == xl.C) && (!mask || ml.ld == xl.C);
   if (!compact) return false;
   const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
+  if (size == 5 && (xl.C == 64 || xl.C == 192)) {
+    const int64_t warps = (npix + 1) / 2;
+    int64_t blocks = (warps * 32 + 255) / 256;
+    if (blocks > (int64_t)WAP_NUM_SMS * 16) blocks = (int64_t)WAP_NUM_SMS * 16;
+    if (xl.C == 64)
+      lrn_warp_kernel<1, BWD><<<(int)blocks, 256, 0, st>>>(x, xl, dy, dyl, alpha, beta, bias, out, ol, mask, ml);
+    else
+      lrn_warp_kernel<3, BWD><<<(int)blocks, 256, 0, st>>>(x, xl, dy, dyl, alpha, beta, bias, out, ol, mask, ml);
+    return true;
+  }
   auto blocks = [&](int pix) { return grid_for(npix, pix); };
   if (xl.C == 64) {
     lrn_fast_kernel<16, 32, BWD><<<blocks(32), 256, 0, st>>>(x, xl, dy, dyl, size, alpha, beta, bias, out, ol, mask, ml);
@@ -723,8 +852,9 @@ extern "C" int wap_bias_grad(const float* dy, wap_layout_t l, float* db, float* 
   const int64_t rows = (int64_t)l.B * (l.H + 2 * l.pad) * (l.W + 2 * l.pad);
   const int chunks = bias_chunks(l);
   const int64_t rpc = (rows + chunks - 1) / chunks;
-  dim3 grid((l.C + 31) / 32, chunks);
-  bias_grad_partial<<<grid, 256, 0, STREAM(stream)>>>(dy, rows, l.ld, l.C, rpc, work);
+  const int cw = bias_cw(l);
+  dim3 grid((l.ld / 4 + cw - 1) / cw, chunks);
+  bias_grad_partial<<<grid, 256, 0, STREAM(stream)>>>(dy, rows, l.ld, l.C, rpc, cw, work);
   WAP_LAUNCH_CHECK();
   bias_grad_final<<<(l.C + 127) / 128, 128, 0, STREAM(stream)>>>(work, chunks, l.ld, l.C, db);
   WAP_LAUNCH_CHECK();
