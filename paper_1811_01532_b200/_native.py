@@ -14,6 +14,9 @@ from pathlib import Path
 from .errors import EvalError, WorkloadError
 
 _LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libwapb200.so"
+# diagnostics only (tools/): load an alternative in-tree build, e.g. a traced GEMM
+if os.environ.get("WAP_LIB_VARIANT"):
+    _LIB_PATH = _LIB_PATH.with_name(f"libwapb200_{os.environ['WAP_LIB_VARIANT']}.so")
 MAX_TAPS = 32
 
 

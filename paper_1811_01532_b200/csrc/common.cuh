@@ -78,7 +78,24 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// Waiters suspend in try_wait (woken by the phase flip, or after the hint)
+// instead of spinning, so idle roles do not steal issue slots from the TMA
+// producer / MMA issuer sharing their SM sub-partition.
+#ifndef WAP_MBAR_HINT
+#define WAP_MBAR_HINT 0x989680
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#if WAP_MBAR_HINT > 0
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "n"(WAP_MBAR_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -88,6 +105,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
+#endif
 }
 
 __device__ __forceinline__ void tma_prefetch(const void* tmap) {

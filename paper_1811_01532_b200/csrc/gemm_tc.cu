@@ -125,6 +125,8 @@ void plan_window(const wap_gemm_desc_t& d, const Shape& s, int& boxes, int& off_
   const wap_operand_t& a = d.a;
   if (d.precision != 3 || a.mn_major || a.tap_period <= 0 || a.ntaps < 2 || d.window < 0) return;
   if ((int64_t)a.ntaps * a.tap_period != d.K) return;
+  // the producer reuses the A tap for a tapped K-major B
+  if (!d.b.mn_major && d.b.tap_period > 0 && d.b.tap_period != a.tap_period) return;
   int mn = a.off[0], mx = a.off[0];
   for (int t = 1; t < a.ntaps; ++t) {
     mn = std::min(mn, (int)a.off[t]);

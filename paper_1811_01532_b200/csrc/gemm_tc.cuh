@@ -23,6 +23,8 @@
 
 #include <cudaTypedefs.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "../../include/wap_b200.h"
 
@@ -32,7 +34,7 @@ constexpr int BM = 128;  // rows per CTA
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row
 constexpr int kSmemBudget = 204 * 1024;  // + 16.5 KB epilogue staging below
 constexpr int kEpiStage = 4 * 32 * 33 * 4;
-constexpr int kBarBytes = 512;  // mbarriers + TMEM address holder
+constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap offsets of A, B [512,768)
 #ifndef WAP_SPLIT_GROUPS
 #define WAP_SPLIT_GROUPS 2
 #endif
@@ -387,6 +389,18 @@ __device__ unsigned long long g_gemm_trace[64];
 #define TRACE_END() do {} while (0)
 #endif
 
+// TMA coordinates of the 32-row box starting at row mn of an MN-major operand:
+// inner coordinate and the k-row offset of its tap (constant along k).
+__device__ __forceinline__ void mn_box(const OperandDev& op, const int32_t* off, int mn, int& c0, int& o) {
+  int tap = 0;
+  if (op.tap_period > 0) {
+    tap = mn / op.tap_period;
+    if (tap >= op.ntaps) tap = op.ntaps - 1;  // rows past M only feed masked outputs
+  }
+  c0 = mn - tap * op.tap_period;
+  o = off[tap];
+}
+
 struct TileCoord {
   int m0, n0, split, kc_begin, kc_end;
 };
@@ -424,6 +438,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
   uint64_t* tfull_bar = bars + 3 * STAGES;      // [2] accumulator ready (MMA commit, multicast)
   uint64_t* tempty_bar = bars + 3 * STAGES + 2; // [2] accumulator drained (leader-side)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+  int32_t(*s_off)[WAP_MAX_TAPS] = reinterpret_cast<int32_t(*)[WAP_MAX_TAPS]>(reinterpret_cast<uint8_t*>(bars) + 512);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -436,17 +451,13 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
   auto stage_a = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES); };
   auto stage_b = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES + C::A_OFF); };
   auto stage_bs = [&](int s) { return smem_u32(smem + s * C::STAGE_BYTES + C::A_OFF + C::B_BYTES); };
-  // WIN: k-chunk kc -> (channel chunk, tap), tap innermost; returns the flat k
+  // WIN: k-chunk kc = (channel chunk, tap), tap innermost
   const int ntaps = WIN ? g.a.ntaps : 1;
-  auto k_of = [&](int kc) {
-    if constexpr (WIN) {
-      const int cidx = kc / ntaps, tap = kc - cidx * ntaps;
-      return tap * g.a.tap_period + cidx * BK;
-    } else {
-      return kc * BK;
-    }
-  };
 
+  if (warp == 3) {
+    s_off[0][lane] = g.a.off[lane];
+    s_off[1][lane] = g.b.off[lane];
+  }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
@@ -480,6 +491,12 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs) ----------------
+      // Coordinates advance incrementally along k: the k loop has no integer
+      // divisions or indexed constant loads (a single thread issues every box,
+      // so its dependent-instruction latency bounds the whole pipeline).
+      constexpr int NA = A_MN ? BM / 32 : 1;
+      constexpr int NB = B_MN ? C::B_ROWS / 32 : 1;
+      const int tpa = g.a.tap_period, tpb = g.b.tap_period;
       int s = 0;
       uint32_t ph = 0;
       int wc = 0;  // windows issued
@@ -487,39 +504,79 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         const TileCoord tc = decode_tile(g, t, BN, CG);
         const int a_row0 = tc.m0 + (int)rank * BM;
         const int b_row0 = tc.n0 + (int)rank * C::B_ROWS;
+        // MN-major operands: the tap of each 32-row box is fixed for the tile
+        int ac0[NA], ao[NA], bc0[NB], bo[NB];
+#pragma unroll
+        for (int j = 0; j < NA; ++j) mn_box(g.a, s_off[0], a_row0 + 32 * j, ac0[j], ao[j]);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) mn_box(g.b, s_off[1], b_row0 + 32 * j, bc0[j], bo[j]);
+        // K-major operands: (tap, k within tap) advance with k
+        int k = tc.kc_begin * BK;
+        int a_tap = 0, a_kin = k, b_tap = 0, b_kin = k;
+        if (tpa > 0) { a_tap = k / tpa; a_kin = k - a_tap * tpa; }
+        if (tpb > 0) { b_tap = k / tpb; b_kin = k - b_tap * tpb; }
+        int a_row = a_row0 + s_off[0][A_MN ? 0 : a_tap], b_row = b_row0 + s_off[1][B_MN ? 0 : b_tap];
+        int w_cidx = 0, w_tap = 0;  // WIN: k-chunk = (channel chunk, tap), tap innermost
+        if constexpr (WIN) { w_cidx = tc.kc_begin / ntaps; w_tap = tc.kc_begin - w_cidx * ntaps; }
         for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc) {
           if constexpr (WIN) {
-            const int cidx = kc / ntaps, tap = kc - cidx * ntaps;
-            if (tap == 0 || kc == tc.kc_begin) {
+            if (w_tap == 0 || kc == tc.kc_begin) {
               const int ws = wc & 1;
               TW(1, mbar_wait(smem_u32(&wempty_bar[ws]), ((wc >> 1) & 1) ^ 1));
               const uint32_t wb = smem_u32(&wfull_bar[ws]);
               mbar_arrive_expect_tx(wb, win_bytes);
-              for (int bx = 0; bx < g.win_boxes; ++bx)
-                tma_load_2d(smem_u32(win_base + ws * win_bytes + bx * C::A_BYTES), &tmA, wb, cidx * BK,
-                            a_row0 + g.win_off_min + bx * BM);
+              TW(3, for (int bx = 0; bx < g.win_boxes; ++bx)
+                tma_load_2d(smem_u32(win_base + ws * win_bytes + bx * C::A_BYTES), &tmA, wb, w_cidx * BK,
+                            a_row0 + g.win_off_min + bx * BM));
               ++wc;
             }
             TW(2, mbar_wait(smem_u32(&empty_bar[s]), ph ^ 1));
             const uint32_t fb = smem_u32(&full_bar[s]);
             mbar_arrive_expect_tx(fb, C::B_BYTES);
-            load_operand<C::B_ROWS, B_MN, 1>(&tmB, g.b, stage_b(s), fb, b_row0, k_of(kc));
+            const int kflat = w_tap * tpa + w_cidx * BK;
+            if constexpr (B_MN) {
+#pragma unroll
+              for (int j = 0; j < NB; ++j) tma_load<1>(stage_b(s) + j * (BK * 128), &tmB, fb, bc0[j], kflat + bo[j]);
+            } else if (tpb > 0) {  // host guarantees tpb == tpa: the B tap is the A tap
+              tma_load<1>(stage_b(s), &tmB, fb, w_cidx * BK, b_row0 + s_off[1][w_tap]);
+            } else {
+              tma_load<1>(stage_b(s), &tmB, fb, kflat, b_row);
+            }
             if (++s == STAGES) { s = 0; ph ^= 1; }
+            if (++w_tap == ntaps) { w_tap = 0; ++w_cidx; }
             continue;
           }
           TW(2, mbar_wait(smem_u32(&empty_bar[s]), ph ^ 1));
           uint32_t fb = smem_u32(&full_bar[s]);
+          auto issue = [&](auto cgt) {
+            constexpr int CGT = decltype(cgt)::value;
+            if constexpr (A_MN) {
+#pragma unroll
+              for (int j = 0; j < NA; ++j) tma_load<CGT>(stage_a(s) + j * (BK * 128), &tmA, fb, ac0[j], k + ao[j]);
+            } else {
+              tma_load<CGT>(stage_a(s), &tmA, fb, a_kin, a_row);
+            }
+            if constexpr (B_MN) {
+#pragma unroll
+              for (int j = 0; j < NB; ++j) tma_load<CGT>(stage_b(s) + j * (BK * 128), &tmB, fb, bc0[j], k + bo[j]);
+            } else {
+              tma_load<CGT>(stage_b(s), &tmB, fb, b_kin, b_row);
+            }
+          };
           if constexpr (CG == 2 && PREC == 1) {
             fb &= 0xFEFFFFFFu;  // the leader's barrier collects both CTAs' bytes
             if (leader) mbar_arrive_expect_tx(fb, 2 * (C::A_BYTES + C::B_BYTES));
-            load_operand<BM, A_MN, 2>(&tmA, g.a, stage_a(s), fb, a_row0, kc * BK);
-            load_operand<C::B_ROWS, B_MN, 2>(&tmB, g.b, stage_b(s), fb, b_row0, kc * BK);
+            issue(std::integral_constant<int, 2>{});
           } else {
             mbar_arrive_expect_tx(fb, C::A_BYTES + C::B_BYTES);
-            load_operand<BM, A_MN, 1>(&tmA, g.a, stage_a(s), fb, a_row0, kc * BK);
-            load_operand<C::B_ROWS, B_MN, 1>(&tmB, g.b, stage_b(s), fb, b_row0, kc * BK);
+            TW(3, issue(std::integral_constant<int, 1>{}));
           }
           if (++s == STAGES) { s = 0; ph ^= 1; }
+          k += BK;
+          a_kin += BK;
+          b_kin += BK;
+          if (!A_MN && tpa > 0 && a_kin >= tpa) { a_kin -= tpa; ++a_tap; a_row = a_row0 + s_off[0][a_tap]; }
+          if (!B_MN && tpb > 0 && b_kin >= tpb) { b_kin -= tpb; ++b_tap; b_row = b_row0 + s_off[1][b_tap]; }
         }
       }
     }
@@ -554,8 +611,13 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           const uint32_t a_big0 = tmem_base + C::A_COL0 + aj * 64;
           const uint32_t first0 = kc > tc.kc_begin ? 1u : 0u;
 #ifdef WAP_GEMM_TMA_ONLY
-          // diagnostic: measure the TMA stream alone (no MMA)
-          if (elect_one()) mbar_arrive(smem_u32(&empty_bar[s]));
+          // diagnostic: measure the TMA (+ split) stream alone, no MMA
+          if (elect_one()) {
+            for (uint32_t r = 0; r < (uint32_t)CG; ++r) {
+              mbar_arrive_cluster(map_to_rank(smem_u32(&empty_bar[s]), r));
+              if constexpr (PREC == 3) mbar_arrive_cluster(map_to_rank(smem_u32(&aslot_bar[aj]), r));
+            }
+          }
           if (false) {
 #else
           if (elect_one()) {
@@ -581,7 +643,8 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           if (++aj == C::A_SLOTS) aj = 0;
         }
 #ifdef WAP_GEMM_TMA_ONLY
-        if (elect_one()) mbar_arrive(smem_u32(&tfull_bar[acc]));
+        if (elect_one())
+          for (uint32_t r = 0; r < (uint32_t)CG; ++r) mbar_arrive_cluster(map_to_rank(smem_u32(&tfull_bar[acc]), r));
 #else
         if (elect_one()) umma_commit_cg<CG>(smem_u32(&tfull_bar[acc]));
 #endif
@@ -701,12 +764,11 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
     bool wwaited = false;        // WIN: this group has waited for the current window
     for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
       const TileCoord tc = decode_tile(g, t, BN, CG);
-      for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc, ++it) {
-        int tap = 0;
+      int tap = 0;  // WIN: tap of the current k-chunk (tap innermost), advanced without division
+      if constexpr (WIN) tap = tc.kc_begin % ntaps;
+      for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc, ++it, tap = (WIN && tap + 1 == ntaps) ? 0 : tap + 1) {
         bool last_in_win = false;
         if constexpr (WIN) {
-          const int cidx = kc / ntaps;
-          tap = kc - cidx * ntaps;
           if (tap == 0 || kc == tc.kc_begin) {
             wslot = wc & 1;
             ++wc;
@@ -721,6 +783,17 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           continue;
         }
         TW(1, mbar_wait(smem_u32(&full_bar[s]), ph));
+#ifdef WAP_GEMM_NO_SPLIT
+        // diagnostic: skip the split work (TMA stream + handshakes only)
+        named_bar_sync(2 + group, 256);
+        if (gt == 0) {
+          if (CG == 2 && !leader) mbar_arrive_cluster(conv_leader + s * 8);
+          else mbar_arrive(smem_u32(&conv_bar[s]));
+          if (WIN && last_in_win) mbar_arrive(smem_u32(&wempty_bar[wslot]));
+        }
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+        continue;
+#endif
         uint8_t* base = smem + s * C::STAGE_BYTES;
         uint32_t v[16], w[16];
         if constexpr (WIN) {
@@ -729,7 +802,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
             wwaited = true;
           }
           // row ct of this tap's tile = window row ct + shift(tap) - min shift
-          load_a_half_kmajor(win_base + wslot * win_bytes, ct + g.a.off[tap] - g.win_off_min, half, v);
+          load_a_half_kmajor(win_base + wslot * win_bytes, ct + s_off[0][tap] - g.win_off_min, half, v);
         } else if constexpr (A_MN) {
           load_a_half_mnmajor(base, ct, half, v);
         } else {
@@ -743,14 +816,14 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         }
         // TMEM A slot of this step: free once the MMAs of its previous use committed
         const int aj = it % C::A_SLOTS;
-        mbar_wait(smem_u32(&aslot_bar[aj]), ((it / C::A_SLOTS) & 1) ^ 1);
+        TW(2, mbar_wait(smem_u32(&aslot_bar[aj]), ((it / C::A_SLOTS) & 1) ^ 1));
         tc_fence_after();
         const uint32_t acol = tmem_base + lane_base + C::A_COL0 + aj * 64 + half * 16;
         tmem_st_32x32b_x16(acol, v);
         tmem_st_32x32b_x16(acol + 32, w);
         split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_OFF),
                          reinterpret_cast<uint32_t*>(base + C::A_OFF + C::B_BYTES), C::B_ROWS * BK, gt, 256);
-        tmem_st_wait();
+        TW(3, tmem_st_wait());
         tc_fence_before();
         fence_proxy_async_smem();
         // one arrival per CTA: group-local named barrier, then a single thread

@@ -14,8 +14,8 @@ from bench import he_init, synthetic_batch  # noqa: E402
 from paper_1811_01532_b200 import _native as N  # noqa: E402
 from paper_1811_01532_b200 import models, planner, trainer  # noqa: E402
 
-ROLES = ["producer(empty-win / empty)", "mma(tempty / conv|full)", "epilogue(tfull)", "splitter0(full / win / bar)",
-         "splitter1(full / win / bar)"]
+ROLES = ["producer(empty-win / empty / tma-issue)", "mma(tempty / conv|full)", "epilogue(tfull)",
+         "splitter0(full / win+aslot / st-wait+bar)", "splitter1(full / win+aslot / st-wait+bar)"]
 
 
 def main():
@@ -40,7 +40,7 @@ def main():
     L.wap_gemm_trace_read(C.cast(buf, C.c_void_p), 20)
     for r in range(5):
         tot = buf[4 * r] or 1
-        print(f"{ROLES[r]:32s} total {buf[4 * r]:>10d} cyc  waits: " +
+        print(f"{ROLES[r]:44s} total {buf[4 * r]:>10d} cyc  waits: " +
               ", ".join(f"{100 * buf[4 * r + i] / tot:5.1f}%" for i in range(1, 4)))
 
 

@@ -2,8 +2,7 @@
 
     python tools/profile_step.py --model alexnet --batch 128 --only d_conv2_w --reps 3
 runs the whole step once (warm-up), then `--reps` times only the steps whose
-name matches `--only` (substring), so `ncu -k regex:gemm_tc -s <warmups>` can
-catch exactly that kernel.
+name matches `--only` (substring), so `ncu --profile-from-start off` catches exactly those launches.
 """
 import argparse
 import sys
@@ -37,6 +36,9 @@ def main():
     sel = [s for s in tr.prog.steps if s.name in names] or [s for s in tr.prog.steps if args.only in s.name]
     print("selected:", [s.name for s in sel], flush=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # ncu --profile-from-start off captures only this region (autotuning and
+    # warm-up launches stay outside it)
+    torch.cuda.profiler.start()
     for i in range(args.reps):
         if i == 1:
             e0.record()
@@ -44,6 +46,7 @@ def main():
             s(N.stream_ptr())
     e1.record()
     torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     if args.reps > 1:
         print(f"avg ms per rep: {e0.elapsed_time(e1) / (args.reps - 1):.4f}", flush=True)
 
