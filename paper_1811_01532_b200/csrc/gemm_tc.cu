@@ -154,6 +154,7 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
   WAP_CHECK_ARG(d.M >= 1 && d.N >= 1 && d.K >= 1, "bad GEMM shape M=%lld N=%lld K=%lld", (long long)d.M,
                 (long long)d.N, (long long)d.K);
   WAP_CHECK_ARG(d.precision == 1 || d.precision == 3, "precision must be 1 (tf32) or 3 (3xtf32)");
+  WAP_CHECK_ARG(d.M < (1LL << 31) && d.N < (1LL << 31), "GEMM extents must stay below 2^31 rows/columns");
   WAP_CHECK_ARG(d.c != nullptr && d.ldc >= d.N, "bad output");
   WAP_CHECK_ARG(!(d.a.mn_major && !d.b.mn_major), "unsupported operand majors (A MN-major, B K-major)");
   int rc;

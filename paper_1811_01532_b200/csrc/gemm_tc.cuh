@@ -33,7 +33,8 @@ namespace wapgemm {
 constexpr int BM = 128;  // rows per CTA
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row
 constexpr int kSmemBudget = 204 * 1024;  // + 16.5 KB epilogue staging below
-constexpr int kEpiStage = 4 * 32 * 33 * 4;
+constexpr int kEpiLd = 36;                    // epilogue staging row stride (floats)
+constexpr int kEpiStage = 4 * 32 * kEpiLd * 4;  // 4 warps x [32 rows][36]
 constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap offsets of A, B [512,768)
 #ifndef WAP_SPLIT_GROUPS
 #define WAP_SPLIT_GROUPS 2
@@ -283,11 +284,22 @@ __device__ __forceinline__ void split_tile(uint32_t* raw, uint32_t* small, int n
   }
 }
 
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ float4 ld_shared_v4f(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ bool halo_row(const GemmArgs& g, int64_t m) {
   if (g.halo_pad <= 0) return false;
   const int hp = g.halo_h + 2 * g.halo_pad, wp = g.halo_w + 2 * g.halo_pad;
-  const int w = (int)(m % wp);
-  const int h = (int)((m / wp) % hp);
+  // padded-grid rows of one launch stay below 2^31 (host-checked), so 32-bit math
+  const int mi = (int)m;
+  const int w = mi % wp;
+  const int h = (mi / wp) % hp;
   return w < g.halo_pad || w >= g.halo_pad + g.halo_w || h < g.halo_pad || h >= g.halo_pad + g.halo_h;
 }
 
@@ -654,23 +666,42 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
     }
   } else if (warp >= 4 && warp < 8) {
     // ---------------- epilogue ----------------
+    // Phase 1 (thread = accumulator row): tcgen05.ld 32 columns, raw values into
+    // this warp's smem block (row stride 36 floats: conflict-free 16-byte accesses).
+    // Phase 2 (coalesced, 4 rows x 128 B per instruction): bias / ReLU / GradReLU
+    // mask / halo zeroing per 4 columns, with the 8 mask loads of a chunk issued
+    // back-to-back, then 16-byte stores.
     const int wq = warp - 4;  // TMEM lane quarter
-    float* stg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes) + wq * (32 * 33);
+    float* stg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes) + wq * (32 * kEpiLd);
+    const uint32_t stg_s = smem_u32(stg);
     const uint32_t tempty_leader = CG == 2 ? map_to_rank(smem_u32(&tempty_bar[0]), 0) : smem_u32(&tempty_bar[0]);
     int acc = 0;
     uint32_t acc_ph = 0;
     const bool vec = (g.ldc % 4) == 0;
+    const bool raw_out = g.partial != nullptr;
+    const float* bias = raw_out ? nullptr : g.bias;
+    const float* mask = raw_out ? nullptr : g.mask;
+    const bool mvec = (g.ldm % 4) == 0;
+    const int c4 = (lane & 7) * 4;
     for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
       const TileCoord tc = decode_tile(g, t, BN, CG);
       TW(1, mbar_wait(smem_u32(&tfull_bar[acc]), acc_ph));
+#ifdef WAP_GEMM_TRACE
+      const unsigned long long _drain0 = clock64();
+#endif
       tc_fence_after();
       const int64_t m_warp = (int64_t)tc.m0 + (int64_t)rank * BM + wq * 32;  // first row of this warp
-      const int64_t m = m_warp + lane;
-      const bool row_ok = m < g.M;
-      const bool halo = row_ok && halo_row(g, m);
-      const bool raw_out = g.partial != nullptr;
       float* out_base = raw_out ? g.partial + (int64_t)tc.split * g.split_stride : g.c;
-      const float* mrow = (g.mask && row_ok) ? g.mask + m * g.ldm : nullptr;
+      // rows this lane stores in phase 2: it * 4 + lane / 8
+      uint32_t row_ok = 0, row_zero = 0;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int64_t row = m_warp + it * 4 + (lane >> 3);
+        if (row < g.M) {
+          row_ok |= 1u << it;
+          if (!raw_out && halo_row(g, row)) row_zero |= 1u << it;
+        }
+      }
 #pragma unroll 1
       for (int cb = 0; cb < BN / 32; ++cb) {
         uint32_t v[32];
@@ -678,67 +709,81 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         tmem_ld_wait();
         const int nb = tc.n0 + cb * 32;
         if (nb >= g.N) continue;  // warp-uniform
-        // 1) per-row epilogue math (thread = row), staged into this warp's smem block
         const bool full = vec && nb + 32 <= g.N;
+        const int col = nb + c4;
+        // 1) raw accumulator row -> smem block
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float x[4] = {__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
-                        __uint_as_float(v[j + 3])};
-          if (!raw_out) {
-            if (g.bias) {
-              if (full) {
-                const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + nb + j));
-                x[0] += b4.x; x[1] += b4.y; x[2] += b4.z; x[3] += b4.w;
-              } else {
+        for (int j = 0; j < 32; j += 4)
+          st_shared_v4(stg_s + (uint32_t)(lane * kEpiLd + j) * 4u, v[j], v[j + 1], v[j + 2], v[j + 3]);
+        __syncwarp();
+        // 2) bias of this lane's 4 columns; mask loads of 4 rows in flight together
+        float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (bias) {
+          if (full) b4 = __ldg(reinterpret_cast<const float4*>(bias + col));
+          else {
+            if (col < g.N) b4.x = __ldg(bias + col);
+            if (col + 1 < g.N) b4.y = __ldg(bias + col + 1);
+            if (col + 2 < g.N) b4.z = __ldg(bias + col + 2);
+            if (col + 3 < g.N) b4.w = __ldg(bias + col + 3);
+          }
+        }
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                  if (nb + j + i < g.N) x[i] += __ldg(g.bias + nb + j + i);
+        for (int hh = 0; hh < 2; ++hh) {
+          float4 mk[4];
+          if (mask) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int it = hh * 4 + i;
+              mk[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (row_ok & (1u << it)) {
+                const float* mp = mask + (m_warp + it * 4 + (lane >> 3)) * g.ldm + col;
+                if (full && mvec) mk[i] = __ldg(reinterpret_cast<const float4*>(mp));
+                else {
+                  if (col < g.N) mk[i].x = __ldg(mp);
+                  if (col + 1 < g.N) mk[i].y = __ldg(mp + 1);
+                  if (col + 2 < g.N) mk[i].z = __ldg(mp + 2);
+                  if (col + 3 < g.N) mk[i].w = __ldg(mp + 3);
+                }
               }
             }
-            if (g.relu) {
-#pragma unroll
-              for (int i = 0; i < 4; ++i) x[i] = fmaxf(x[i], 0.f);
-            }
-            if (mrow) {
-              float mk[4];
-              if (full && (g.ldm % 4) == 0) {
-                const float4 m4 = __ldg(reinterpret_cast<const float4*>(mrow + nb + j));
-                mk[0] = m4.x; mk[1] = m4.y; mk[2] = m4.z; mk[3] = m4.w;
-              } else {
-#pragma unroll
-                for (int i = 0; i < 4; ++i) mk[i] = (nb + j + i < g.N) ? __ldg(mrow + nb + j + i) : 0.f;
-              }
-#pragma unroll
-              for (int i = 0; i < 4; ++i) x[i] = mk[i] > 0.f ? x[i] : 0.f;
-            }
-            if (halo) x[0] = x[1] = x[2] = x[3] = 0.f;
           }
 #pragma unroll
-          for (int i = 0; i < 4; ++i) stg[lane * 33 + j + i] = x[i];
-        }
-        __syncwarp();
-        // 2) coalesced stores: each instruction writes 4 rows x 128 contiguous bytes
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int r = it * 4 + (lane >> 3);
-          const int c4 = (lane & 7) * 4;
-          const int64_t row = m_warp + r;
-          if (row < g.M) {
-            float* dst = out_base + row * g.ldc + nb + c4;
-            const float* src = stg + r * 33 + c4;
+          for (int i = 0; i < 4; ++i) {
+            const int it = hh * 4 + i;
+            if (!(row_ok & (1u << it))) continue;
+            const int r = it * 4 + (lane >> 3);
+            float4 x = ld_shared_v4f(stg_s + (uint32_t)(r * kEpiLd + c4) * 4u);
+            if (!raw_out) {
+              x.x += b4.x; x.y += b4.y; x.z += b4.z; x.w += b4.w;
+              if (g.relu) {
+                x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+              }
+              if (mask) {
+                x.x = mk[i].x > 0.f ? x.x : 0.f;
+                x.y = mk[i].y > 0.f ? x.y : 0.f;
+                x.z = mk[i].z > 0.f ? x.z : 0.f;
+                x.w = mk[i].w > 0.f ? x.w : 0.f;
+              }
+              if (row_zero & (1u << it)) x = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            float* dst = out_base + (m_warp + r) * g.ldc + col;
             if (full) {
-              *reinterpret_cast<float4*>(dst) = make_float4(src[0], src[1], src[2], src[3]);
+              *reinterpret_cast<float4*>(dst) = x;
             } else {
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                if (nb + c4 + i < g.N) dst[i] = src[i];
+              if (col < g.N) dst[0] = x.x;
+              if (col + 1 < g.N) dst[1] = x.y;
+              if (col + 2 < g.N) dst[2] = x.z;
+              if (col + 3 < g.N) dst[3] = x.w;
             }
           }
         }
         __syncwarp();
       }
       tc_fence_before();
-      named_bar_sync(1, 128);
+      TW(3, named_bar_sync(1, 128));
+#ifdef WAP_GEMM_TRACE
+      _tr[2] += clock64() - _drain0;
+#endif
       if (wq == 0 && lane == 0) {
         if (CG == 2 && !leader) mbar_arrive_cluster(tempty_leader + acc * 8);
         else mbar_arrive(smem_u32(&tempty_bar[acc]));

@@ -14,7 +14,7 @@ from bench import he_init, synthetic_batch  # noqa: E402
 from paper_1811_01532_b200 import _native as N  # noqa: E402
 from paper_1811_01532_b200 import models, planner, trainer  # noqa: E402
 
-ROLES = ["producer(empty-win / empty / tma-issue)", "mma(tempty / conv|full)", "epilogue(tfull)",
+ROLES = ["producer(empty-win / empty / tma-issue)", "mma(tempty / conv|full)", "epilogue(tfull / drain / drain-bar)",
          "splitter0(full / win+aslot / st-wait+bar)", "splitter1(full / win+aslot / st-wait+bar)"]
 
 
