@@ -437,7 +437,9 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
   using C = Cfg<BN, PREC, CG, WIN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base derived from smem_raw by pointer arithmetic, so the
+  // compiler keeps the shared address space (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* win_base = smem + STAGES * C::STAGE_BYTES;                  // 2 A halo windows (WIN)
   const int win_bytes = WIN ? g.win_boxes * C::A_BYTES : 0;
   uint64_t* bars = reinterpret_cast<uint64_t*>(win_base + 2 * win_bytes);
