@@ -35,12 +35,30 @@ UNIT = "images/sec"
 DEFAULT_BATCH = {"alexnet": 128, "vgg16": 32}
 
 
+# tcgen05.mma kind::tf32 issue rate measured on this pool's B200 by tools/mma_probe.cu
+# (profiles/r01/mma_probe.txt: 2048 MAC/clk/SM for N >= 128 = 1116 TFLOP/s; nominal 1.1 PF).
+# MEASURED_PEAKS.json carries only HBM and bf16 figures, so the TF32 GEMM roofline uses this.
+TF32_MMA_PEAK_TFLOPS = 1116.4
+
+
 def peaks():
+    """(HBM GB/s, bf16 TFLOP/s, source) from the driver-written MEASURED_PEAKS.json, else the
+    fallback of /opt/skills/guides/B200_PROFILING.md."""
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+        return float(d.get("hbm_gbs", 6650.0)), float(d.get("bf16_tflops", 1590.0)), "measured"
     return 6650.0, 1590.0, "fallback"
+
+
+def traffic_of(model: str, step: str):
+    """DRAM bytes per launch of `step` from the committed ncu --set full captures
+    (profiles/traffic.json, written by tools/capture_traffic.sh), or None."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    e = json.loads(p.read_text()).get(model, {}).get(step)
+    return None if e is None else int(e["traffic_bytes"])
 
 
 class ClockSampler:
@@ -58,7 +76,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -210,8 +228,13 @@ def run_ours(args, rank, world, local_rank):
     gemm_flops = sum(s.alg_flops for _, s in gemms)
     dom_ms, dom = max(gemms, key=lambda x: x[0])
     hbm_peak, bf16_peak, peak_src = peaks()
-    tf32_peak = bf16_peak / 2.0  # dense TF32 runs at half the bf16 tensor rate
+    tf32_peak = TF32_MMA_PEAK_TFLOPS
     pipe_factor = 3 if args.precision == 3 else 1
+    # HBM-bound kernels (im2col, pool, LRN, bias-grad, xent, SGD): algorithmic bytes / event time
+    ew = [(v[0], v[1]) for v in per.values() if getattr(v[1], "alg_bytes", 0) > 0]
+    ew_ms = sum(m for m, _ in ew)
+    ew_bytes = sum(st.alg_bytes for _, st in ew)
+    ew_top = sorted(ew, key=lambda x: -x[0])[:6]
     achieved = dom.alg_flops * pipe_factor / (dom_ms * 1e-3) / 1e12
     launches = prog.launches_per_step() if not tr._captured else _count_launches(prog)
 
@@ -233,12 +256,25 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": launches * args.steps,
             "roofline": {"bound": "tensor", "kernel": dom.name, "gemm_shape_MNK": list(dom.shape),
                          "achieved": round(achieved, 2), "peak": tf32_peak, "unit": "TFLOP/s",
-                         "frac": round(achieved / tf32_peak, 4), "traffic": None,
-                         "peak_note": f"TF32 dense = {peak_src} bf16 burst / 2; achieved counts tensor-pipe FLOPs "
-                                      f"({pipe_factor}x algorithmic for {'3xTF32' if pipe_factor == 3 else 'TF32'})",
+                         "frac": round(achieved / tf32_peak, 4), "traffic": traffic_of(args.model, dom.name),
+                         "algorithmic_flops": dom.alg_flops,
+                         "peak_note": "measured tcgen05 kind::tf32 issue rate (tools/mma_probe.cu, "
+                                      "profiles/r01/mma_probe.txt); achieved counts tensor-pipe FLOPs "
+                                      f"({pipe_factor}x algorithmic for {'3xTF32' if pipe_factor == 3 else 'TF32'}); "
+                                      "traffic = ncu dram bytes per launch (profiles/traffic.json)",
                          "kernel_ms": round(dom_ms, 4), "share_of_step": round(dom_ms / total_kernel_ms, 4)},
             "gemm_summary": {"ms": round(gemm_ms, 3), "share": round(gemm_ms / total_kernel_ms, 4),
-                             "algorithmic_tflops": round(gemm_flops / (gemm_ms * 1e-3) / 1e12, 2)},
+                             "algorithmic_tflops": round(gemm_flops / (gemm_ms * 1e-3) / 1e12, 2),
+                             "tensor_pipe_frac": round(gemm_flops * pipe_factor / (gemm_ms * 1e-3) / 1e12
+                                                       / tf32_peak, 4)},
+            "hbm_summary": {"ms": round(ew_ms, 3), "share": round(ew_ms / total_kernel_ms, 4),
+                            "achieved_gbs": round(ew_bytes / (ew_ms * 1e-3) / 1e9, 1) if ew_ms else None,
+                            "peak_gbs": hbm_peak, "peak_src": peak_src,
+                            "frac": round(ew_bytes / (ew_ms * 1e-3) / 1e9 / hbm_peak, 4) if ew_ms else None,
+                            "top": [{"kernel": st.name, "ms": round(m, 4),
+                                     "gbs": round(st.alg_bytes / (m * 1e-3) / 1e9, 1),
+                                     "frac": round(st.alg_bytes / (m * 1e-3) / 1e9 / hbm_peak, 4)}
+                                    for m, st in ew_top]},
         }
         if args.breakdown:
             out["breakdown_ms"] = {k: round(v[0], 4) for k, v in sorted(per.items(), key=lambda x: -x[1][0])}
@@ -318,12 +354,14 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: 128 AlexNet, 32 VGG-16)")
     ap.add_argument("--precision", type=int, default=3, choices=[1, 3])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-batch", type=int, default=4)
+    ap.add_argument("--ref-batch", type=int, default=0,
+                    help="images per reference step (default: 4 AlexNet, 1 VGG-16, ~2-4 s of host work each)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    args.ref_batch = args.ref_batch or (4 if args.model == "alexnet" else 1)
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -346,7 +384,8 @@ def main():
     if rank == 0:
         out["clocks"] = clocks
         if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(args.model, 2 if args.model == "alexnet" else 1)
+            # a bounded sample (~10-20 s of host work): one fp64 step at a reduced batch
+            out["cpu_baseline"] = cpu_baseline(args.model, 16 if args.model == "alexnet" else 4)
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -124,6 +124,7 @@ class Step:
     args: tuple
     what: str = ""
     keep: list = field(default_factory=list)  # objects that must outlive the step (plans, ctypes arrays)
+    alg_bytes: int = 0  # algorithmic HBM bytes per launch (each logical element read/written once)
 
     def __call__(self, stream: int) -> None:
         rc = self.fn(*self.args, stream) if self.fn is not None else 0
@@ -446,8 +447,13 @@ class Program:
                 self.t[zb] = self.t[r]  # mask source: relu(x) > 0  <=>  x > 0
 
     # ---------------------------------------------------------------- lowering
-    def _emit(self, name, fn, args, what="", keep=None):
-        self.steps.append(Step(name, fn, tuple(args), what, keep or []))
+    def _emit(self, name, fn, args, what="", keep=None, alg_bytes=0):
+        self.steps.append(Step(name, fn, tuple(args), what, keep or [], int(alg_bytes)))
+
+    @staticmethod
+    def _nbytes(*tensors) -> int:
+        """fp32 bytes of the logical elements of `tensors` (halo and lane padding excluded)."""
+        return sum(4 * int(np.prod(t.dims)) for t in tensors if t is not None)
 
     def _gemm(self, name, M, Nn, K, a, b, out: Tensor, bias=None, relu=False, mask: Tensor | None = None,
               halo=(0, 0, 0), splits=0, to_updates=False):
@@ -483,65 +489,72 @@ class Program:
 
     def _lower(self) -> None:
         L = self.L
+        self.step_end: dict[str, int] = {}  # node id -> number of steps emitted once it is lowered
         for nid in self.order:
-            n = self.node(nid)
-            k = n.kind
-            if k in (OpKind.INPUT, OpKind.VARIABLE):
-                continue
-            if k is OpKind.CONV2D:
-                self._lower_conv(n)
-            elif k is OpKind.MATMUL:
-                self._lower_matmul(n)
-            elif k is OpKind.BIAS_ADD:
-                if self.node(n.inputs[0]).id in self.fwd_fuse:
-                    continue  # fused into the GEMM epilogue
-                self._elementwise(0, n.inputs[0], None, n.inputs[1], nid)
-            elif k is OpKind.RELU:
-                if n.inputs[0] in self.mask_alias and self.mask_alias[n.inputs[0]] == nid:
-                    continue  # fused
-                self._elementwise(1, n.inputs[0], None, None, nid)
-            elif k is OpKind.GRAD_RELU:
-                if nid in self.bwd_mask.values():
-                    continue  # written by the fused producer
-                self._elementwise(3, n.inputs[1], self.mask_src(n.inputs[0]), None, nid)
-            elif k in (OpKind.SOFTMAX_XENT_LOSS, OpKind.GRAD_SOFTMAX_XENT):
-                self._lower_xent(n)
-            elif k is OpKind.GRAD_BIAS:
-                self._lower_bias_grad(n)
-            elif k is OpKind.GRAD_MATMUL_W:
-                self._lower_matmul_w(n)
-            elif k is OpKind.GRAD_MATMUL_X:
-                self._lower_matmul_x(n)
-            elif k is OpKind.GRAD_CONV2D_W:
-                self._lower_conv_w(n)
-            elif k is OpKind.GRAD_CONV2D_X:
-                self._lower_conv_x(n)
-            elif k is OpKind.MAX_POOL:
-                self._lower_pool(n)
-            elif k is OpKind.GRAD_MAX_POOL:
-                self._lower_pool_grad(n)
-            elif k is OpKind.LRN:
-                self._lower_lrn(n)
-            elif k is OpKind.GRAD_LRN:
-                self._lower_lrn_grad(n)
-            elif k in (OpKind.ADD_N,):
-                self._lower_add_n(n)
-            elif k is OpKind.ALL_REDUCE_SUM:
-                self._lower_allreduce(n)
-            elif k is OpKind.SPLIT:
-                pass  # resolved by consumers (see _in)
-            elif k is OpKind.CONCAT:
-                self._lower_concat(n)
-            elif k is OpKind.SGD_UPDATE:
-                self._lower_sgd(n)
-            else:
-                raise EvalError(f"no GPU rule for kind {k.value}")
+            self._lower_node(nid)
+            self.step_end[nid] = len(self.steps)
         if self.autotune:
             self._autotune_gemms()
         self._schedule_collectives()
         self._fuse_updates()
         self.steps.extend(self.update_steps)
         self.update_steps = []
+
+    def _lower_node(self, nid: str) -> None:
+        """Lower one graph node to its launch step(s)."""
+        L = self.L
+        n = self.node(nid)
+        k = n.kind
+        if k in (OpKind.INPUT, OpKind.VARIABLE):
+            return
+        if k is OpKind.CONV2D:
+            self._lower_conv(n)
+        elif k is OpKind.MATMUL:
+            self._lower_matmul(n)
+        elif k is OpKind.BIAS_ADD:
+            if self.node(n.inputs[0]).id in self.fwd_fuse:
+                return  # fused into the GEMM epilogue
+            self._elementwise(0, n.inputs[0], None, n.inputs[1], nid)
+        elif k is OpKind.RELU:
+            if n.inputs[0] in self.mask_alias and self.mask_alias[n.inputs[0]] == nid:
+                return  # fused
+            self._elementwise(1, n.inputs[0], None, None, nid)
+        elif k is OpKind.GRAD_RELU:
+            if nid in self.bwd_mask.values():
+                return  # written by the fused producer
+            self._elementwise(3, n.inputs[1], self.mask_src(n.inputs[0]), None, nid)
+        elif k in (OpKind.SOFTMAX_XENT_LOSS, OpKind.GRAD_SOFTMAX_XENT):
+            self._lower_xent(n)
+        elif k is OpKind.GRAD_BIAS:
+            self._lower_bias_grad(n)
+        elif k is OpKind.GRAD_MATMUL_W:
+            self._lower_matmul_w(n)
+        elif k is OpKind.GRAD_MATMUL_X:
+            self._lower_matmul_x(n)
+        elif k is OpKind.GRAD_CONV2D_W:
+            self._lower_conv_w(n)
+        elif k is OpKind.GRAD_CONV2D_X:
+            self._lower_conv_x(n)
+        elif k is OpKind.MAX_POOL:
+            self._lower_pool(n)
+        elif k is OpKind.GRAD_MAX_POOL:
+            self._lower_pool_grad(n)
+        elif k is OpKind.LRN:
+            self._lower_lrn(n)
+        elif k is OpKind.GRAD_LRN:
+            self._lower_lrn_grad(n)
+        elif k in (OpKind.ADD_N,):
+            self._lower_add_n(n)
+        elif k is OpKind.ALL_REDUCE_SUM:
+            self._lower_allreduce(n)
+        elif k is OpKind.SPLIT:
+            pass  # resolved by consumers (see _in)
+        elif k is OpKind.CONCAT:
+            self._lower_concat(n)
+        elif k is OpKind.SGD_UPDATE:
+            self._lower_sgd(n)
+        else:
+            raise EvalError(f"no GPU rule for kind {k.value}")
 
     def _autotune_gemms(self, reps: int = 3) -> None:
         """Per-GEMM launch configuration by measurement: one CTA vs a CTA pair
@@ -558,10 +571,14 @@ class Program:
             best, best_ms = st.call, None
             a = st.desc.a
             windows = (0, -1) if (self.precision == 3 and not a.mn_major and a.ntaps > 1) else (0,)
-            for cluster, window in [(c, w) for c in (1, 2) for w in windows]:
+            # BN = 128 keeps two TMEM accumulators in 3xTF32 (epilogue overlaps the next tile),
+            # wider tiles halve B traffic: measure both where N allows
+            bns = (0, 128) if (self.precision == 3 and st.desc.N >= 192) else (0,)
+            for cluster, window, bn in [(c, w, b) for c in (1, 2) for w in windows for b in bns]:
                 d = type(st.desc).from_buffer_copy(st.desc)
                 d.cluster = cluster
                 d.window = window
+                d.block_n = bn
                 d.workspace, d.workspace_bytes = None, 0
                 try:
                     call = GemmCall(d, device=self.device)
@@ -608,9 +625,26 @@ class Program:
         side = self.torch.cuda.Stream(device=self.device)
         self.comm_stream = side
         inserts: dict[int, list] = {}
+        # SGD of a bucket also runs on the comm stream, right behind its allreduce,
+        # once the last backward kernel reading those weights (GradMatMulX /
+        # GradConv2DX) has been issued: the update overlaps the rest of backward.
+        lr = self._uniform_lr()
+        self.bucket_sgd = self.in_place and lr is not None
+        var_of_slot = {self.arena_off[v]: v for v in self.arena_off}
         for ready, lo, hi, ids in buckets:
+            buf = self.grad_arena[lo:hi]
             inserts.setdefault(ready, []).append(
-                _BucketStep("+".join(ids), self.collective, self.grad_arena[lo:hi], side, self.torch))
+                _BucketStep("+".join(ids), self.collective, buf, side, self.torch))
+            if self.bucket_sgd:
+                vars_in = [v for o, v in var_of_slot.items() if lo <= o < hi]
+                readers = [self.step_end[u] for v in vars_in for u in self.users[v]
+                           if self.kind(u) is not OpKind.SGD_UPDATE]
+                at = max([ready] + readers)
+                sgd = Step(f"sgd[{lo}:{hi}]", self.L.wap_sgd,
+                           (self.var_arena[lo:hi].data_ptr(), buf.data_ptr(), C.c_float(lr),
+                            self.var_arena[lo:hi].data_ptr(), hi - lo), "SgdUpdate (bucket)",
+                           alg_bytes=12 * (hi - lo))
+                inserts.setdefault(at, []).append(_SideStep(sgd, side, self.torch))
         new_steps = []
         for i, st in enumerate(self.steps):
             new_steps.extend(inserts.get(i, []))
@@ -620,19 +654,31 @@ class Program:
         self.steps = new_steps
         self.buckets = [(lo * 4, hi * 4, ids) for _, lo, hi, ids in buckets]
 
+    def _uniform_lr(self):
+        lrs = {float(self.node(u).attr("learning_rate")) for u in self.updates}
+        return lrs.pop() if len(lrs) == 1 else None
+
     def _fuse_updates(self) -> None:
         """In-place training: one SGD launch over the whole variable arena when all
         updates share a learning rate (variables without an update have a zero
-        gradient slot, so w - lr*0 leaves them unchanged)."""
+        gradient slot, so w - lr*0 leaves them unchanged). With cross-rank
+        buckets the updates already ran per bucket on the comm stream."""
         if not self.in_place or not self.update_steps:
             return
-        lrs = {float(self.node(u).attr("learning_rate")) for u in self.updates}
-        if len(lrs) != 1 or any(not isinstance(s, Step) for s in self.update_steps):
+        if getattr(self, "bucket_sgd", False) and self.buckets:
+            covered = sum(hi - lo for lo, hi, _ in self.buckets) // 4
+            upd_vars = {self.node(u).inputs[0] for u in self.updates}
+            if covered and all(any(lo // 4 <= self.arena_off[v] < hi // 4 for lo, hi, _ in self.buckets)
+                               for v in upd_vars):
+                self.update_steps = []
+                return
+        lr = self._uniform_lr()
+        if lr is None or any(not isinstance(s, Step) for s in self.update_steps):
             return
-        lr = lrs.pop()
         self.update_steps = [Step("sgd(arena)", self.L.wap_sgd,
                                   (self.var_arena.data_ptr(), self.grad_arena.data_ptr(), C.c_float(lr),
-                                   self.var_arena.data_ptr(), self.arena_numel), "SgdUpdate (fused arena)")]
+                                   self.var_arena.data_ptr(), self.arena_numel), "SgdUpdate (fused arena)",
+                                  alg_bytes=12 * self.arena_numel)]
 
     # -- tensor access ---------------------------------------------------------
     def _in(self, consumer: Node, nid: str) -> Tensor:
@@ -685,7 +731,8 @@ class Program:
             col = self.torch.empty(rows * ldcol, dtype=self.torch.float32, device=self.device)
             self.t[f"{n.id}::col"] = Tensor((rows, K), 0, ldcol, col, "mat")
             self._emit(n.id + "/im2col", self.L.wap_im2col,
-                       (x.ptr, x.layout(), kk, s, p, ho, wo, P, col.data_ptr(), ldcol), "im2col")
+                       (x.ptr, x.layout(), kk, s, p, ho, wo, P, col.data_ptr(), ldcol), "im2col",
+                       alg_bytes=self._nbytes(x) + 4 * b * ho * wo * K)
             ct = self.t[f"{n.id}::col"]
             a = self._operand(ct, False, inner=K)
             bo = N.operand(w.ptr, inner=co, outer=K, ld=w.ld, mn_major=True)
@@ -714,7 +761,8 @@ class Program:
         al = self._as_compat(aux, y)[0] if aux is not None else N.wap_layout_t()
         self._emit(out_id, self.L.wap_elementwise,
                    (op, x.ptr, xl, aux.ptr if aux is not None else None, al,
-                    bias.ptr if bias is not None else None, y.ptr, yl), f"elementwise[{op}] {out_id}")
+                    bias.ptr if bias is not None else None, y.ptr, yl), f"elementwise[{op}] {out_id}",
+                   alg_bytes=self._nbytes(x, aux, bias, y))
 
     @staticmethod
     def _as_compat(a: Tensor, b: Tensor):
@@ -754,7 +802,7 @@ class Program:
         work = self.torch.empty(rows, dtype=self.torch.float32, device=self.device)
         self._emit(n.id + "/xent", self.L.wap_xent_fwd_bwd,
                    (z.ptr, z.ld, y.ptr, y.ld, rows, cols, C.c_float(float(denom)), loss.ptr, dz.ptr, dz.ld,
-                    work.data_ptr()), "softmax-xent", keep=[work, loss, dz])
+                    work.data_ptr()), "softmax-xent", keep=[work, loss, dz], alg_bytes=12 * rows * cols)
 
     def _lower_bias_grad(self, n: Node) -> None:
         dy = self._in(n, n.inputs[0])
@@ -762,7 +810,8 @@ class Program:
         lay = dy.layout()
         wf = self.L.wap_bias_grad_work_floats(lay)
         work = self.torch.empty(max(wf, 1), dtype=self.torch.float32, device=self.device)
-        self._emit(n.id, self.L.wap_bias_grad, (dy.ptr, lay, db.ptr, work.data_ptr()), "GradBias", keep=[work])
+        self._emit(n.id, self.L.wap_bias_grad, (dy.ptr, lay, db.ptr, work.data_ptr()), "GradBias", keep=[work],
+                   alg_bytes=self._nbytes(dy, db))
 
     # -- backward GEMMs ------------------------------------------------------
     def _lower_matmul_w(self, n: Node) -> None:
@@ -826,7 +875,8 @@ class Program:
             ml = mask.layout() if mask is not None else N.wap_layout_t()
             self._emit(n.id + "/col2im", self.L.wap_col2im,
                        (dcol.data_ptr(), ldcol, kk, s, p, ho, wo, P, out.ptr, out.layout(),
-                        mask.ptr if mask is not None else None, ml), "col2im", keep=[dcol])
+                        mask.ptr if mask is not None else None, ml), "col2im", keep=[dcol],
+                       alg_bytes=4 * b * ho * wo * K + self._nbytes(out, mask))
 
     def _lower_conv_w(self, n: Node) -> None:
         x = self._in(n, n.inputs[0])
@@ -862,7 +912,7 @@ class Program:
         self.t[f"{n.id}::argmax"] = Tensor(y.dims, y.pad, y.ld, arg, "nhwc")
         self._emit(n.id, self.L.wap_maxpool_fwd,
                    (x.ptr, x.layout(), n.attr("window"), n.attr("stride"), y.ptr, y.layout(), arg.data_ptr()),
-                   "MaxPool", keep=[arg])
+                   "MaxPool", keep=[arg], alg_bytes=self._nbytes(x, y) + self._nbytes(y) // 4)
 
     def _lower_pool_grad(self, n: Node) -> None:
         x_id, dy_id = n.inputs
@@ -879,7 +929,8 @@ class Program:
             raise EvalError("MaxPool gradient must share the pooled output layout")
         self._emit(n.id, self.L.wap_maxpool_bwd,
                    (arg.ptr, dy.ptr, dy.layout(), n.attr("window"), n.attr("stride"), out.ptr, out.layout(),
-                    mask.ptr if mask is not None else None, ml), "GradMaxPool")
+                    mask.ptr if mask is not None else None, ml), "GradMaxPool",
+                   alg_bytes=self._nbytes(dy, out, mask) + self._nbytes(dy) // 4)
 
     def _lower_lrn(self, n: Node) -> None:
         x = self._in(n, n.inputs[0])
@@ -887,7 +938,7 @@ class Program:
         a = n.attrs
         self._emit(n.id, self.L.wap_lrn_fwd,
                    (x.ptr, x.layout(), a["size"], C.c_float(a["alpha"]), C.c_float(a["beta"]), C.c_float(a["bias"]),
-                    y.ptr, y.layout()), "LRN")
+                    y.ptr, y.layout()), "LRN", alg_bytes=self._nbytes(x, y))
 
     def _lower_lrn_grad(self, n: Node) -> None:
         x = self._in(n, n.inputs[0])
@@ -900,7 +951,7 @@ class Program:
         self._emit(n.id, self.L.wap_lrn_bwd,
                    (x.ptr, x.layout(), dy.ptr, dy.layout(), a["size"], C.c_float(a["alpha"]), C.c_float(a["beta"]),
                     C.c_float(a["bias"]), out.ptr, out.layout(), mask.ptr if mask is not None else None, ml),
-                   "GradLRN")
+                   "GradLRN", alg_bytes=self._nbytes(x, dy, out, mask))
 
     # -- aggregation / update ------------------------------------------------
     def _lower_add_n(self, n: Node) -> None:
@@ -1064,6 +1115,26 @@ class _BucketStep(_CollectiveStep):
         self.side.wait_event(ev)
         with torch.cuda.stream(self.side):
             self.fn(self.buf)
+
+
+class _SideStep(_CollectiveStep):
+    """A native step issued on the comm stream after the compute stream reaches it."""
+
+    def __init__(self, step, side, torch):
+        self.name = step.name
+        self.step = step
+        self.alg_bytes = step.alg_bytes
+        self.side = side
+        self.torch = torch
+
+    def __call__(self, stream: int) -> None:
+        torch = self.torch
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.side.wait_event(ev)
+        from . import _native as N
+
+        self.step(N.stream_ptr(self.side))
 
 
 class _JoinStep(_CollectiveStep):

@@ -1,6 +1,6 @@
 """Two ranks on one B200 (gloo on CUDA tensors): each rank runs its rank view of
 the WAP-transformed graph through Trainer (bucketed allreduce on a side stream,
-fused arena SGD, in-place variables). The updated variables and per-rank losses
+each bucket's SGD behind its allreduce on that stream, in-place variables). The updated variables and per-rank losses
 must match a single-process GPU execution of the full transformed graph."""
 
 import os
@@ -57,7 +57,8 @@ def _worker(rank, world, port, net, kw, q):
         shard = {k: torch.from_numpy(np.ascontiguousarray(bind[k][rank * b:(rank + 1) * b]).astype(np.float32))
                  for k in ("images", "labels")}
         loss = tr.step(shard, fetch=True)
-        q.put((rank, loss, tr.variables(), len(tr.prog.buckets)))
+        sgd_on_comm = tr.prog.bucket_sgd and not any(st.name == "sgd(arena)" for st in tr.prog.steps)
+        q.put((rank, loss, tr.variables(), len(tr.prog.buckets), sgd_on_comm))
     finally:
         dist.destroy_process_group()
 
@@ -77,8 +78,9 @@ def test_two_ranks_match_single_process(cuda, net, kw):
         p.start()
     res = {}
     for _ in range(world):
-        r, loss, var, nb = q.get(timeout=600)
+        r, loss, var, nb, sgd_on_comm = q.get(timeout=600)
         res[r] = (loss, var, nb)
+        assert sgd_on_comm, "bucket SGD should run on the comm stream behind each allreduce"
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0

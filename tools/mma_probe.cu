@@ -52,7 +52,7 @@ __device__ __forceinline__ void commit(uint32_t bar) {
 }
 
 // smem: A tile 128 x 32 fp32 (16 KB) + B tile 256 x 32 fp32 (32 KB), K-major SW128
-template <int N, int CG, bool TS>
+template <int N, int CG, bool TS, int NACC = 1>
 __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* cycles) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
@@ -91,8 +91,10 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* c
       if (tid == 0) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          if constexpr (TS) mma_ts<CG>(tmem, a_tmem + kk * 8, bd + kk * 2, idesc, (it | kk) ? 1u : 0u);
-          else mma_ss<CG>(tmem, ad + kk * 2, bd + kk * 2, idesc, (it | kk) ? 1u : 0u);
+          // NACC independent accumulators (columns [j*N, j*N+N)) break the RAW chain on D
+          const uint32_t d = tmem + (uint32_t)((kk % NACC) * N);
+          if constexpr (TS) mma_ts<CG>(d, a_tmem + kk * 8, bd + kk * 2, idesc, (it | kk) ? 1u : 0u);
+          else mma_ss<CG>(d, ad + kk * 2, bd + kk * 2, idesc, (it | kk) ? 1u : 0u);
         }
       }
       __syncwarp();
@@ -118,9 +120,9 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* c
   }
 }
 
-template <int N, int CG, bool TS>
+template <int N, int CG, bool TS, int NACC = 1>
 void run(int iters) {
-  auto k = probe<N, CG, TS>;
+  auto k = probe<N, CG, TS, NACC>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 50 * 1024);
   unsigned long long* cyc;
   cudaMalloc(&cyc, 8);
@@ -155,14 +157,21 @@ void run(int iters) {
     const double mac_clk_sm = macs_per_leader / cyc_per / CG;
     const double tflops = 2.0 * macs_per_leader * leaders / (ms * 1e-3) / 1e12;
     if (rep == 1)
-      printf("%s cta_group::%d N=%3d: %7.1f MAC/clk/SM  (%5.1f clk per MMA)  %6.1f TFLOP/s  (%.3f ms)\n",
-             TS ? "TS" : "SS", CG, N, mac_clk_sm, cyc_per / (iters * 4.0), tflops, ms);
+      printf("%s acc=%d cta_group::%d N=%3d: %7.1f MAC/clk/SM  (%5.1f clk per MMA)  %6.1f TFLOP/s  (%.3f ms)\n",
+             TS ? "TS" : "SS", NACC, CG, N, mac_clk_sm, cyc_per / (iters * 4.0), tflops, ms);
   }
   cudaFree(cyc);
 }
 
 int main() {
   const int iters = 20000;
+  // independent accumulators at small N (A in TMEM at column 256: N * NACC <= 256)
+  run<64, 1, true, 2>(iters);
+  run<64, 1, true, 4>(iters);
+  run<64, 2, true, 2>(iters);
+  run<64, 2, true, 4>(iters);
+  run<64, 1, false, 2>(iters);
+  run<128, 2, true, 2>(iters);
   run<64, 1, false>(iters);
   run<128, 1, false>(iters);
   run<256, 1, false>(iters);
