@@ -137,19 +137,24 @@ int bias_cw(const wap_layout_t& l) {
   return cols4 >= 32 ? 32 : (cols4 >= 16 ? 16 : (cols4 >= 8 ? 8 : (cols4 >= 4 ? 4 : (cols4 >= 2 ? 2 : 1))));
 }
 
+// One warp per column: lanes take chunks lane, lane + 32, ... and the warp
+// reduces in a fixed shuffle order (deterministic for a fixed chunk count).
 __global__ void bias_grad_final(const float* __restrict__ part, int chunks, int ld, int C, float* __restrict__ db) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
   if (c >= C) return;
   float s = 0.f;
-  for (int k = 0; k < chunks; ++k) s += part[(int64_t)k * ld + c];
-  db[c] = s;
+  for (int k = lane; k < chunks; k += 32) s += part[(int64_t)k * ld + c];
+  s = warp_sum(s);
+  if (lane == 0) db[c] = s;
 }
 
 int bias_chunks(const wap_layout_t& l) {
   const int64_t rows = (int64_t)l.B * (l.H + 2 * l.pad) * (l.W + 2 * l.pad);
   const int cw = bias_cw(l);
   const int ctiles = (l.ld / 4 + cw - 1) / cw;
-  int64_t chunks = (2 * WAP_NUM_SMS + ctiles - 1) / ctiles;
+  // enough blocks (8 per SM) to keep ~64 KB of loads in flight per SM
+  int64_t chunks = (8 * WAP_NUM_SMS + ctiles - 1) / ctiles;
   const int64_t max_chunks = (rows + 63) / 64;
   if (chunks > max_chunks) chunks = max_chunks;
   if (chunks < 1) chunks = 1;
@@ -191,7 +196,7 @@ __global__ void im2col_kernel(const float* __restrict__ x, wap_layout_t xl, int 
 // Table-driven im2col: a block owns IM2COL_ROWS output rows; the (u, v, c)
 // decode of every column is computed once per block into shared memory, so the
 // inner loop is a table lookup + one coalesced store per element.
-constexpr int IM2COL_ROWS = 16;
+constexpr int IM2COL_ROWS = 32;
 constexpr int IM2COL_MAXK = 4096;
 
 __global__ void __launch_bounds__(256) im2col_table_kernel(const float* __restrict__ x, wap_layout_t xl, int k, int s,
@@ -200,6 +205,7 @@ __global__ void __launch_bounds__(256) im2col_table_kernel(const float* __restri
   __shared__ short tu[IM2COL_MAXK], tv[IM2COL_MAXK];
   __shared__ int toff[IM2COL_MAXK];
   __shared__ int rb[IM2COL_ROWS], rh[IM2COL_ROWS], rw[IM2COL_ROWS];
+  __shared__ int64_t rbase[IM2COL_ROWS];
   const int C = xl.C;
   const int K = k * k * C;
   const int Wxp = xl.W + 2 * xl.pad;
@@ -213,31 +219,54 @@ __global__ void __launch_bounds__(256) im2col_table_kernel(const float* __restri
   const int Hp = Ho + 2 * P, Wp = Wo + 2 * P;
   __syncthreads();
   if (ldcol % 4 == 0) {
-    // flat float4 mapping: 4 consecutive columns of one row per thread (a float4
-    // never straddles rows since ldcol % 4 == 0); row decoded once per float4
-    const int64_t total4 = M * ldcol / 4;
+    // float4 path: a block sweeps IM2COL_ROWS rows at a time; row geometry comes
+    // from a per-row smem table (decoded once per row), columns from the per-block
+    // tap table, and the element index is 32-bit (no 64-bit division in the loop).
     const int q4 = (int)(ldcol / 4);
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total4; e += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t m = e / q4;
-      const int kk0 = (int)(e - m * q4) * 4;
-      const int wo = (int)(m % Wp) - P;
-      const int64_t q = m / Wp;
-      const int ho = (int)(q % Hp) - P;
-      const int b = (int)(q / Hp);
-      float o[4] = {0.f, 0.f, 0.f, 0.f};
-      if (ho >= 0 && ho < Ho && wo >= 0 && wo < Wo) {
-        const int h0 = ho * s - p, w0 = wo * s - p;
-        const int64_t base = (((int64_t)b * (xl.H + 2 * xl.pad) + h0 + xl.pad) * Wxp + w0 + xl.pad) * xl.ld;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int kk = kk0 + i;
-          if (kk < K) {
-            const int hi = h0 + tu[kk], wi = w0 + tv[kk];
-            if (hi >= 0 && hi < xl.H && wi >= 0 && wi < xl.W) o[i] = __ldg(x + base + toff[kk]);
+    for (int64_t r0 = (int64_t)blockIdx.x * IM2COL_ROWS; r0 < M; r0 += (int64_t)gridDim.x * IM2COL_ROWS) {
+      __syncthreads();
+      if (threadIdx.x < IM2COL_ROWS) {
+        const int64_t m = r0 + threadIdx.x;
+        int64_t base = 0;  // may be negative: taps outside the image are masked per element
+        int h0 = 0, w0 = 0, valid = 0;
+        if (m < M) {
+          const int wo = (int)(m % Wp) - P;
+          const int64_t q = m / Wp;
+          const int ho = (int)(q % Hp) - P;
+          const int bb = (int)(q / Hp);
+          if (ho >= 0 && ho < Ho && wo >= 0 && wo < Wo) {
+            h0 = ho * s - p;
+            w0 = wo * s - p;
+            base = (((int64_t)bb * (xl.H + 2 * xl.pad) + h0 + xl.pad) * Wxp + w0 + xl.pad) * xl.ld;
+            valid = 1;
           }
         }
+        rb[threadIdx.x] = valid;
+        rh[threadIdx.x] = h0;
+        rw[threadIdx.x] = w0;
+        rbase[threadIdx.x] = base;
       }
-      reinterpret_cast<float4*>(col)[e] = make_float4(o[0], o[1], o[2], o[3]);
+      __syncthreads();
+      const int nrows = (M - r0) < IM2COL_ROWS ? (int)(M - r0) : IM2COL_ROWS;
+      float4* out4 = reinterpret_cast<float4*>(col + r0 * ldcol);
+      for (int idx = threadIdx.x; idx < nrows * q4; idx += blockDim.x) {
+        const int r = idx / q4;
+        const int kk0 = (idx - r * q4) * 4;
+        float o[4] = {0.f, 0.f, 0.f, 0.f};
+        if (rb[r]) {
+          const int h0 = rh[r], w0 = rw[r];
+          const float* xb = x + rbase[r];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int kk = kk0 + i;
+            if (kk < K) {
+              const int hi = h0 + tu[kk], wi = w0 + tv[kk];
+              if (hi >= 0 && hi < xl.H && wi >= 0 && wi < xl.W) o[i] = __ldg(xb + toff[kk]);
+            }
+          }
+        }
+        out4[idx] = make_float4(o[0], o[1], o[2], o[3]);
+      }
     }
     return;
   }
@@ -856,7 +885,7 @@ extern "C" int wap_bias_grad(const float* dy, wap_layout_t l, float* db, float* 
   dim3 grid((l.ld / 4 + cw - 1) / cw, chunks);
   bias_grad_partial<<<grid, 256, 0, STREAM(stream)>>>(dy, rows, l.ld, l.C, rpc, cw, work);
   WAP_LAUNCH_CHECK();
-  bias_grad_final<<<(l.C + 127) / 128, 128, 0, STREAM(stream)>>>(work, chunks, l.ld, l.C, db);
+  bias_grad_final<<<(l.C + 3) / 4, 128, 0, STREAM(stream)>>>(work, chunks, l.ld, l.C, db);
   WAP_LAUNCH_CHECK();
   g_wap_launches.fetch_add(2, std::memory_order_relaxed);
   return WAP_OK;
