@@ -190,6 +190,22 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
   p->win = g.win_boxes > 0 ? 1 : 0;
   g.partial = nullptr;
   g.split_stride = d.M * d.ldc;
+  // epilogue output through bulk tensor stores when C is TMA-addressable
+  g.tma_store = 0;
+  if (s.splits == 1 && (reinterpret_cast<uintptr_t>(d.c) & 15) == 0 && d.ldc % 4 == 0 &&
+      !getenv("WAP_GEMM_NO_TMA_STORE")) {
+    wap_operand_t oc{};
+    oc.ptr = d.c;
+    oc.inner = d.N;
+    oc.outer = d.M;
+    oc.ld = d.ldc;
+    oc.mn_major = 0;
+    oc.ntaps = 1;
+    if ((rc = make_tmap(&p->tmC, oc, 32))) return rc;
+    g.tma_store = 1;
+  } else {
+    p->tmC = p->tmA;  // unused
+  }
   if (s.splits > 1) {
     const int64_t need = (int64_t)s.splits * d.M * d.ldc * 4;
     WAP_CHECK_ARG(d.workspace != nullptr && d.workspace_bytes >= need,

@@ -33,9 +33,15 @@ namespace wapgemm {
 constexpr int BM = 128;  // rows per CTA
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row
 constexpr int kSmemBudget = 204 * 1024;  // + 16.5 KB epilogue staging below
-constexpr int kEpiLd = 36;                    // epilogue staging row stride (floats)
-constexpr int kEpiStage = 4 * 32 * kEpiLd * 4;  // 4 warps x [32 rows][36]
+// epilogue staging: per warp one [32 rows][32 fp32] block in the SWIZZLE_128B
+// layout (16-byte chunk j of row r at chunk j ^ (r & 7)): conflict-free for the
+// row-per-thread writes and the coalesced reads, and the TMA store's source format
+constexpr int kEpiStage = 4 * 32 * 128;
 constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap offsets of A, B [512,768)
+// fewest TMEM A slots (3xTF32) worth keeping two accumulators for
+#ifndef WAP_MIN_A_SLOTS
+#define WAP_MIN_A_SLOTS 4
+#endif
 #ifndef WAP_SPLIT_GROUPS
 #define WAP_SPLIT_GROUPS 2
 #endif
@@ -61,6 +67,7 @@ struct GemmArgs {
   int64_t ldm;
   int32_t halo_pad, halo_h, halo_w;
   int32_t win_boxes, win_off_min;  // WIN: 128-row TMA boxes per A halo window, min tap shift
+  int32_t tma_store;               // epilogue writes C through tmC (bulk tensor stores)
 };
 
 // 3xTF32 keeps the A operand in TMEM (tcgen05 "TS" form): the splitter warps
@@ -84,7 +91,7 @@ struct Cfg {
   // PREC 3 smem stage: [A raw] | B raw | B small
   static constexpr int STAGE_BYTES = PREC == 3 ? (A_OFF + 2 * B_BYTES) : (A_BYTES + B_BYTES);
   // two accumulators (epilogue overlap) only if >= 4 A stages still fit in TMEM
-  static constexpr int ACC_BUFS = (PREC == 3 && 512 - 2 * BN < 4 * 64) ? 1 : 2;
+  static constexpr int ACC_BUFS = (PREC == 3 && 512 - 2 * BN < WAP_MIN_A_SLOTS * 64) ? 1 : 2;
   static constexpr int A_COL0 = ACC_BUFS * BN;
   static constexpr int TMEM_A_SLOTS = PREC == 3 ? (512 - A_COL0) / 64 : 64;
   static constexpr int STAGES_SMEM = kSmemBudget / STAGE_BYTES;
@@ -93,7 +100,7 @@ struct Cfg {
   static constexpr int STAGES = WIN ? 6 : (STAGES_SMEM > 8 ? 8 : STAGES_SMEM);
   static constexpr int TMEM_COLS = PREC == 3 ? 512 : ((2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512));
   static constexpr int THREADS = PREC == 3 ? 256 + 256 * kSplitGroups : 256;  // + splitter warp groups
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + kBarBytes + kEpiStage;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + kEpiStage + kBarBytes;
   static_assert(STAGES >= 2, "need at least two pipeline stages");
   static_assert(B_ROWS % 32 == 0, "B rows per CTA must be a multiple of 32");
 };
@@ -293,6 +300,19 @@ __device__ __forceinline__ float4 ld_shared_v4f(uint32_t addr) {
   return v;
 }
 
+// TMA store smem -> global (bulk group), completion tracked per issuing thread
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tm)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ bool halo_row(const GemmArgs& g, int64_t m) {
   if (g.halo_pad <= 0) return false;
   const int hp = g.halo_h + 2 * g.halo_pad, wp = g.halo_w + 2 * g.halo_pad;
@@ -395,7 +415,16 @@ __device__ unsigned long long g_gemm_trace[64];
       for (int _i = 1; _i < 4; ++_i) g_gemm_trace[_role * 4 + _i] = _tr[_i];                  \
     }                                                                                         \
   } while (0)
+#ifdef WAP_EPI_TRACE  // epilogue split: slot 1 TMEM load, 2 staging, 3 bias/mask/stores
+#define EPI_T0() unsigned long long _e = clock64()
+#define EPI_T(slot) do { const unsigned long long _n = clock64(); _tr[slot] += _n - _e; _e = _n; } while (0)
 #else
+#define EPI_T0() do {} while (0)
+#define EPI_T(slot) do {} while (0)
+#endif
+#else
+#define EPI_T0() do {} while (0)
+#define EPI_T(slot) do {} while (0)
 #define TRACE_BEGIN() do {} while (0)
 #define TW(slot, expr) expr
 #define TRACE_END() do {} while (0)
@@ -433,7 +462,7 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& g, int t, int B
 template <int BN, bool A_MN, bool B_MN, int PREC, int CG, bool WIN = false>
 __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ GemmArgs g) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ GemmArgs g) {
   using C = Cfg<BN, PREC, CG, WIN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -442,7 +471,8 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* win_base = smem + STAGES * C::STAGE_BYTES;                  // 2 A halo windows (WIN)
   const int win_bytes = WIN ? g.win_boxes * C::A_BYTES : 0;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(win_base + 2 * win_bytes);
+  uint8_t* epi_base = win_base + 2 * win_bytes;                        // 1024-aligned staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + kEpiStage);
   uint64_t* wfull_bar = bars + 3 * STAGES + 5;   // [2] window landed (WIN)
   uint64_t* wempty_bar = bars + 3 * STAGES + 7;  // [2] window consumed by both splitter groups (WIN)
   uint64_t* aslot_bar = bars + 3 * STAGES + 9;   // [A_SLOTS] TMEM A slot free again (MMA commit)
@@ -669,26 +699,37 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
   } else if (warp >= 4 && warp < 8) {
     // ---------------- epilogue ----------------
     // Phase 1 (thread = accumulator row): tcgen05.ld 32 columns, raw values into
-    // this warp's smem block (row stride 36 floats: conflict-free 16-byte accesses).
+    // this warp's [32 x 32] smem block (SWIZZLE_128B: conflict-free 16-byte accesses).
     // Phase 2 (coalesced, 4 rows x 128 B per instruction): bias / ReLU / GradReLU
-    // mask / halo zeroing per 4 columns, with the 8 mask loads of a chunk issued
-    // back-to-back, then 16-byte stores.
+    // mask / halo zeroing per 4 columns, with the mask loads of 4 rows in flight
+    // together; the result goes back to the block and leaves through one TMA
+    // bulk tensor store (split-K partial slabs: direct 16-byte stores).
     const int wq = warp - 4;  // TMEM lane quarter
-    float* stg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes) + wq * (32 * kEpiLd);
-    const uint32_t stg_s = smem_u32(stg);
+    const uint32_t stg_s = smem_u32(epi_base) + wq * (32 * 128);
+    // 16-byte chunk q of staged row r (SWIZZLE_128B)
+    auto stg_at = [&](int r, int q) { return stg_s + (uint32_t)(r * 128 + ((q ^ (r & 7)) << 4)); };
     const uint32_t tempty_leader = CG == 2 ? map_to_rank(smem_u32(&tempty_bar[0]), 0) : smem_u32(&tempty_bar[0]);
     int acc = 0;
     uint32_t acc_ph = 0;
     const bool vec = (g.ldc % 4) == 0;
     const bool raw_out = g.partial != nullptr;
+    const bool tma_out = !raw_out && g.tma_store;
+#ifdef WAP_DIAG_NO_BIAS
+    const float* bias = nullptr;
+#else
     const float* bias = raw_out ? nullptr : g.bias;
+#endif
     const float* mask = raw_out ? nullptr : g.mask;
     const bool mvec = (g.ldm % 4) == 0;
     const int c4 = (lane & 7) * 4;
     for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
       const TileCoord tc = decode_tile(g, t, BN, CG);
+#ifdef WAP_EPI_TRACE
+      mbar_wait(smem_u32(&tfull_bar[acc]), acc_ph);
+#else
       TW(1, mbar_wait(smem_u32(&tfull_bar[acc]), acc_ph));
-#ifdef WAP_GEMM_TRACE
+#endif
+#if defined(WAP_GEMM_TRACE) && !defined(WAP_EPI_TRACE)
       const unsigned long long _drain0 = clock64();
 #endif
       tc_fence_after();
@@ -707,17 +748,22 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
 #pragma unroll 1
       for (int cb = 0; cb < BN / 32; ++cb) {
         uint32_t v[32];
+        EPI_T0();
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN + cb * 32, v);
         tmem_ld_wait();
+        EPI_T(1);
         const int nb = tc.n0 + cb * 32;
         if (nb >= g.N) continue;  // warp-uniform
         const bool full = vec && nb + 32 <= g.N;
         const int col = nb + c4;
         // 1) raw accumulator row -> smem block
-#pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          st_shared_v4(stg_s + (uint32_t)(lane * kEpiLd + j) * 4u, v[j], v[j + 1], v[j + 2], v[j + 3]);
+        // the TMA store of the previous chunk must have read the staging block
+        if (tma_out) bulk_wait_read_all();
         __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) st_shared_v4(stg_at(lane, j >> 2), v[j], v[j + 1], v[j + 2], v[j + 3]);
+        __syncwarp();
+        EPI_T(2);
         // 2) bias of this lane's 4 columns; mask loads of 4 rows in flight together
         float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (bias) {
@@ -729,61 +775,123 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
             if (col + 3 < g.N) b4.w = __ldg(bias + col + 3);
           }
         }
+        if (tma_out) {
+          // straight-line: 2 rows at a time, loads / math / stores interleaved by the
+          // compiler (no per-row branches; rows >= M are clipped by the TMA store)
+          const bool relu = g.relu != 0;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          float4 mk[4];
-          if (mask) {
+          for (int hh = 0; hh < 4; ++hh) {
+            float4 mk[2], xs[2];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int it = hh * 4 + i;
-              mk[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (row_ok & (1u << it)) {
+            for (int i = 0; i < 2; ++i) {
+              const int it = hh * 2 + i;
+              mk[i] = make_float4(1.f, 1.f, 1.f, 1.f);
+              if (mask && (row_ok & (1u << it))) {
                 const float* mp = mask + (m_warp + it * 4 + (lane >> 3)) * g.ldm + col;
                 if (full && mvec) mk[i] = __ldg(reinterpret_cast<const float4*>(mp));
                 else {
-                  if (col < g.N) mk[i].x = __ldg(mp);
-                  if (col + 1 < g.N) mk[i].y = __ldg(mp + 1);
-                  if (col + 2 < g.N) mk[i].z = __ldg(mp + 2);
-                  if (col + 3 < g.N) mk[i].w = __ldg(mp + 3);
+                  mk[i].x = col < g.N ? __ldg(mp) : 0.f;
+                  mk[i].y = col + 1 < g.N ? __ldg(mp + 1) : 0.f;
+                  mk[i].z = col + 2 < g.N ? __ldg(mp + 2) : 0.f;
+                  mk[i].w = col + 3 < g.N ? __ldg(mp + 3) : 0.f;
                 }
               }
             }
-          }
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int it = hh * 4 + i;
-            if (!(row_ok & (1u << it))) continue;
-            const int r = it * 4 + (lane >> 3);
-            float4 x = ld_shared_v4f(stg_s + (uint32_t)(r * kEpiLd + c4) * 4u);
-            if (!raw_out) {
+            for (int i = 0; i < 2; ++i) xs[i] = ld_shared_v4f(stg_at((hh * 2 + i) * 4 + (lane >> 3), lane & 7));
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const bool z = (row_zero >> (hh * 2 + i)) & 1u;
+              float4 x = xs[i];
               x.x += b4.x; x.y += b4.y; x.z += b4.z; x.w += b4.w;
-              if (g.relu) {
+              if (relu) {
                 x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
               }
-              if (mask) {
-                x.x = mk[i].x > 0.f ? x.x : 0.f;
-                x.y = mk[i].y > 0.f ? x.y : 0.f;
-                x.z = mk[i].z > 0.f ? x.z : 0.f;
-                x.w = mk[i].w > 0.f ? x.w : 0.f;
-              }
-              if (row_zero & (1u << it)) x = make_float4(0.f, 0.f, 0.f, 0.f);
+              x.x = (!z && mk[i].x > 0.f) ? x.x : 0.f;
+              x.y = (!z && mk[i].y > 0.f) ? x.y : 0.f;
+              x.z = (!z && mk[i].z > 0.f) ? x.z : 0.f;
+              x.w = (!z && mk[i].w > 0.f) ? x.w : 0.f;
+              st_shared_v4(stg_at((hh * 2 + i) * 4 + (lane >> 3), lane & 7), __float_as_uint(x.x),
+                           __float_as_uint(x.y), __float_as_uint(x.z), __float_as_uint(x.w));
             }
-            float* dst = out_base + (m_warp + r) * g.ldc + col;
-            if (full) {
-              *reinterpret_cast<float4*>(dst) = x;
-            } else {
-              if (col < g.N) dst[0] = x.x;
-              if (col + 1 < g.N) dst[1] = x.y;
-              if (col + 2 < g.N) dst[2] = x.z;
-              if (col + 3 < g.N) dst[3] = x.w;
+          }
+        } else {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            float4 mk[4];
+            if (mask) {
+  #pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int it = hh * 4 + i;
+                mk[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (row_ok & (1u << it)) {
+                  const float* mp = mask + (m_warp + it * 4 + (lane >> 3)) * g.ldm + col;
+                  if (full && mvec) mk[i] = __ldg(reinterpret_cast<const float4*>(mp));
+                  else {
+                    if (col < g.N) mk[i].x = __ldg(mp);
+                    if (col + 1 < g.N) mk[i].y = __ldg(mp + 1);
+                    if (col + 2 < g.N) mk[i].z = __ldg(mp + 2);
+                    if (col + 3 < g.N) mk[i].w = __ldg(mp + 3);
+                  }
+                }
+              }
+            }
+  #pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int it = hh * 4 + i;
+              if (!(row_ok & (1u << it))) continue;
+              const int r = it * 4 + (lane >> 3);
+              float4 x = ld_shared_v4f(stg_at(r, lane & 7));
+              if (!raw_out) {
+                x.x += b4.x; x.y += b4.y; x.z += b4.z; x.w += b4.w;
+                if (g.relu) {
+                  x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+                }
+                if (mask) {
+                  x.x = mk[i].x > 0.f ? x.x : 0.f;
+                  x.y = mk[i].y > 0.f ? x.y : 0.f;
+                  x.z = mk[i].z > 0.f ? x.z : 0.f;
+                  x.w = mk[i].w > 0.f ? x.w : 0.f;
+                }
+                if (row_zero & (1u << it)) x = make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+              if (tma_out) {
+                st_shared_v4(stg_at(r, lane & 7), __float_as_uint(x.x), __float_as_uint(x.y), __float_as_uint(x.z),
+                             __float_as_uint(x.w));
+                continue;
+              }
+              float* dst = out_base + (m_warp + r) * g.ldc + col;
+              if (full) {
+                *reinterpret_cast<float4*>(dst) = x;
+              } else {
+                if (col < g.N) dst[0] = x.x;
+                if (col + 1 < g.N) dst[1] = x.y;
+                if (col + 2 < g.N) dst[2] = x.z;
+                if (col + 3 < g.N) dst[3] = x.w;
+              }
             }
           }
         }
+        if (tma_out) {
+          // the whole 32 x 32 block leaves through one bulk tensor store (rows >= M
+          // and columns >= N are clipped by the tensor map)
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, stg_s, nb, (int)m_warp);
+            bulk_commit();
+          }
+        }
         __syncwarp();
+        EPI_T(3);
       }
       tc_fence_before();
+#ifdef WAP_EPI_TRACE
+      named_bar_sync(1, 128);
+#else
       TW(3, named_bar_sync(1, 128));
-#ifdef WAP_GEMM_TRACE
+#endif
+#if defined(WAP_GEMM_TRACE) && !defined(WAP_EPI_TRACE)
       _tr[2] += clock64() - _drain0;
 #endif
       if (wq == 0 && lane == 0) {
@@ -792,6 +900,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
       }
       if (++acc == C::ACC_BUFS) { acc = 0; acc_ph ^= 1; }
     }
+    if (lane == 0) bulk_wait_all();
   } else if (PREC == 3 && warp >= 8) {
     // ---------------- 3xTF32 operand split (both CTAs) ----------------
     // kSplitGroups groups of 8 warps alternate stages. Within a group, warp
@@ -896,7 +1005,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
 __global__ void splitk_reduce_kernel(const GemmArgs g, int splits);
 
 struct Plan {
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmC;
   GemmArgs args;
   int grid;
   int bn, a_mn, b_mn, prec, cg, splits, win;
@@ -940,7 +1049,7 @@ int launch(const Plan& p, cudaStream_t st) {
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  WAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.args));
+  WAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.tmC, p.args));
   return WAP_OK;
 }
 
