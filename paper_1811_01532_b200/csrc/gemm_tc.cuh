@@ -722,8 +722,24 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
     const float* mask = raw_out ? nullptr : g.mask;
     const bool mvec = (g.ldm % 4) == 0;
     const int c4 = (lane & 7) * 4;
+    // bias of this lane's 4 columns of the chunk starting at column nb
+    auto load_bias = [&](int nb) {
+      float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (bias) {
+        const int col = nb + c4;
+        if (vec && nb + 32 <= g.N) b = __ldg(reinterpret_cast<const float4*>(bias + col));
+        else {
+          if (col < g.N) b.x = __ldg(bias + col);
+          if (col + 1 < g.N) b.y = __ldg(bias + col + 1);
+          if (col + 2 < g.N) b.z = __ldg(bias + col + 2);
+          if (col + 3 < g.N) b.w = __ldg(bias + col + 3);
+        }
+      }
+      return b;
+    };
     for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
       const TileCoord tc = decode_tile(g, t, BN, CG);
+      float4 b4_next = load_bias(tc.n0);  // in flight across the accumulator wait
 #ifdef WAP_EPI_TRACE
       mbar_wait(smem_u32(&tfull_bar[acc]), acc_ph);
 #else
@@ -764,57 +780,61 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         for (int j = 0; j < 32; j += 4) st_shared_v4(stg_at(lane, j >> 2), v[j], v[j + 1], v[j + 2], v[j + 3]);
         __syncwarp();
         EPI_T(2);
-        // 2) bias of this lane's 4 columns; mask loads of 4 rows in flight together
-        float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (bias) {
-          if (full) b4 = __ldg(reinterpret_cast<const float4*>(bias + col));
-          else {
-            if (col < g.N) b4.x = __ldg(bias + col);
-            if (col + 1 < g.N) b4.y = __ldg(bias + col + 1);
-            if (col + 2 < g.N) b4.z = __ldg(bias + col + 2);
-            if (col + 3 < g.N) b4.w = __ldg(bias + col + 3);
-          }
-        }
+        // 2) bias of this lane's 4 columns (prefetched one chunk ahead); mask loads of
+        //    the rows in flight together
+        const float4 b4 = b4_next;
+        if (cb + 1 < BN / 32 && nb + 32 < g.N) b4_next = load_bias(nb + 32);
         if (tma_out) {
-          // straight-line: 2 rows at a time, loads / math / stores interleaved by the
-          // compiler (no per-row branches; rows >= M are clipped by the TMA store)
+#ifndef WAP_DIAG_NO_EPI_MATH
+          // 2 rows per iteration, rolled (unrolling lets the compiler hoist 8 rows of
+          // mask addresses out of the chunk loop and spill them); rows >= M are clipped
+          // by the TMA store. Staged row r = it * 4 + lane / 8 has swizzle phase r & 7,
+          // which alternates between two values for even / odd it.
           const bool relu = g.relu != 0;
-#pragma unroll
-          for (int hh = 0; hh < 4; ++hh) {
-            float4 mk[2], xs[2];
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const int it = hh * 2 + i;
-              mk[i] = make_float4(1.f, 1.f, 1.f, 1.f);
-              if (mask && (row_ok & (1u << it))) {
-                const float* mp = mask + (m_warp + it * 4 + (lane >> 3)) * g.ldm + col;
-                if (full && mvec) mk[i] = __ldg(reinterpret_cast<const float4*>(mp));
-                else {
-                  mk[i].x = col < g.N ? __ldg(mp) : 0.f;
-                  mk[i].y = col + 1 < g.N ? __ldg(mp + 1) : 0.f;
-                  mk[i].z = col + 2 < g.N ? __ldg(mp + 2) : 0.f;
-                  mk[i].w = col + 3 < g.N ? __ldg(mp + 3) : 0.f;
-                }
+          const int64_t ldm4 = (int64_t)g.ldm * 4;
+          const float* mp = mask ? mask + (m_warp + (lane >> 3)) * g.ldm + col : nullptr;
+          const uint32_t q = lane & 7, r0 = lane >> 3;
+          const uint32_t s_even = stg_s + r0 * 128 + ((q ^ r0) << 4);
+          const uint32_t s_odd = stg_s + (r0 + 4) * 128 + ((q ^ (r0 + 4)) << 4);
+#pragma unroll 1
+          for (int it = 0; it < 8; it += 2, mp += mask ? 2 * ldm4 : 0) {
+            float4 mk0 = make_float4(1.f, 1.f, 1.f, 1.f), mk1 = mk0;
+            if (mask) {
+              const bool ok0 = row_ok & (1u << it), ok1 = row_ok & (2u << it);
+              if (full && mvec) {
+                if (ok0) mk0 = __ldg(reinterpret_cast<const float4*>(mp));
+                if (ok1) mk1 = __ldg(reinterpret_cast<const float4*>(mp + ldm4));
+              } else {
+                mk0.x = (ok0 && col < g.N) ? __ldg(mp) : 0.f;
+                mk0.y = (ok0 && col + 1 < g.N) ? __ldg(mp + 1) : 0.f;
+                mk0.z = (ok0 && col + 2 < g.N) ? __ldg(mp + 2) : 0.f;
+                mk0.w = (ok0 && col + 3 < g.N) ? __ldg(mp + 3) : 0.f;
+                mk1.x = (ok1 && col < g.N) ? __ldg(mp + ldm4) : 0.f;
+                mk1.y = (ok1 && col + 1 < g.N) ? __ldg(mp + ldm4 + 1) : 0.f;
+                mk1.z = (ok1 && col + 2 < g.N) ? __ldg(mp + ldm4 + 2) : 0.f;
+                mk1.w = (ok1 && col + 3 < g.N) ? __ldg(mp + ldm4 + 3) : 0.f;
               }
             }
-#pragma unroll
-            for (int i = 0; i < 2; ++i) xs[i] = ld_shared_v4f(stg_at((hh * 2 + i) * 4 + (lane >> 3), lane & 7));
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const bool z = (row_zero >> (hh * 2 + i)) & 1u;
-              float4 x = xs[i];
+            const uint32_t a0 = s_even + it * 512, a1 = s_odd + it * 512;
+            float4 x0 = ld_shared_v4f(a0), x1 = ld_shared_v4f(a1);
+            const bool z0 = (row_zero >> it) & 1u, z1 = (row_zero >> (it + 1)) & 1u;
+            auto fin = [&](float4 x, const float4& m, bool z) {
               x.x += b4.x; x.y += b4.y; x.z += b4.z; x.w += b4.w;
               if (relu) {
                 x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
               }
-              x.x = (!z && mk[i].x > 0.f) ? x.x : 0.f;
-              x.y = (!z && mk[i].y > 0.f) ? x.y : 0.f;
-              x.z = (!z && mk[i].z > 0.f) ? x.z : 0.f;
-              x.w = (!z && mk[i].w > 0.f) ? x.w : 0.f;
-              st_shared_v4(stg_at((hh * 2 + i) * 4 + (lane >> 3), lane & 7), __float_as_uint(x.x),
-                           __float_as_uint(x.y), __float_as_uint(x.z), __float_as_uint(x.w));
-            }
+              x.x = (!z && m.x > 0.f) ? x.x : 0.f;
+              x.y = (!z && m.y > 0.f) ? x.y : 0.f;
+              x.z = (!z && m.z > 0.f) ? x.z : 0.f;
+              x.w = (!z && m.w > 0.f) ? x.w : 0.f;
+              return x;
+            };
+            x0 = fin(x0, mk0, z0);
+            x1 = fin(x1, mk1, z1);
+            st_shared_v4(a0, __float_as_uint(x0.x), __float_as_uint(x0.y), __float_as_uint(x0.z), __float_as_uint(x0.w));
+            st_shared_v4(a1, __float_as_uint(x1.x), __float_as_uint(x1.y), __float_as_uint(x1.z), __float_as_uint(x1.w));
           }
+#endif
         } else {
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
@@ -878,7 +898,9 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
+#ifndef WAP_DIAG_NO_EPI_STORE
             tma_store_2d(&tmC, stg_s, nb, (int)m_warp);
+#endif
             bulk_commit();
           }
         }
