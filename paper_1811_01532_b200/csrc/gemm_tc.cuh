@@ -997,8 +997,10 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         TW(2, mbar_wait(smem_u32(&aslot_bar[aj]), ((it / C::A_SLOTS) & 1) ^ 1));
         tc_fence_after();
         const uint32_t acol = tmem_base + lane_base + C::A_COL0 + aj * 64 + half * 16;
+#ifndef WAP_DIAG_NO_A_SPLIT
         tmem_st_32x32b_x16(acol, v);
         tmem_st_32x32b_x16(acol + 32, w);
+#endif
         split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_OFF),
                          reinterpret_cast<uint32_t*>(base + C::A_OFF + C::B_BYTES), C::B_ROWS * BK, gt, 256);
         TW(3, tmem_st_wait());
