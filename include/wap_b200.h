@@ -125,6 +125,13 @@ int wap_bias_grad(const float* dy, wap_layout_t l, float* db, float* work, void*
  * the stored argmax, optionally times [mask > 0] (fused GradReLU). */
 int wap_maxpool_fwd(const float* x, wap_layout_t xl, int window, int stride, float* y, wap_layout_t yl,
                     uint8_t* argmax, void* stream);
+/* Same with flags. WAP_POOL_RELU_FUSED: x is a ReLU output whose GradReLU is fused
+ * into this pool's backward; windows with max <= 0 store argmax 0xFF ("no
+ * gradient"), which equals the GradReLU mask at the argmax element, so the fused
+ * backward runs with mask == NULL. */
+#define WAP_POOL_RELU_FUSED 1
+int wap_maxpool_fwd_ex(const float* x, wap_layout_t xl, int window, int stride, float* y, wap_layout_t yl,
+                       uint8_t* argmax, int flags, void* stream);
 int wap_maxpool_bwd(const uint8_t* argmax, const float* dy, wap_layout_t dyl, int window, int stride,
                     float* dx, wap_layout_t dxl, const float* mask, wap_layout_t ml, void* stream);
 /* LRN across channels: y = x / (bias + alpha * sum_{|j-c|<=size/2} x_j^2)^beta. */

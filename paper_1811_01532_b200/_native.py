@@ -18,6 +18,7 @@ _LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libwapb200.so"
 if os.environ.get("WAP_LIB_VARIANT"):
     _LIB_PATH = _LIB_PATH.with_name(f"libwapb200_{os.environ['WAP_LIB_VARIANT']}.so")
 MAX_TAPS = 32
+POOL_RELU_FUSED = 1  # include/wap_b200.h WAP_POOL_RELU_FUSED
 
 
 class NativeUnavailable(RuntimeError):
@@ -130,6 +131,7 @@ _SIGNATURES: list[tuple[str, object, list]] = [
     ("wap_bias_grad_work_floats", _I64, [wap_layout_t]),
     ("wap_bias_grad", _I, [_P, wap_layout_t, _P, _P, _P]),
     ("wap_maxpool_fwd", _I, [_P, wap_layout_t, _I, _I, _P, wap_layout_t, _P, _P]),
+    ("wap_maxpool_fwd_ex", _I, [_P, wap_layout_t, _I, _I, _P, wap_layout_t, _P, _I, _P]),
     ("wap_maxpool_bwd", _I, [_P, _P, wap_layout_t, _I, _I, _P, wap_layout_t, _P, wap_layout_t, _P]),
     ("wap_lrn_fwd", _I, [_P, wap_layout_t, _I, _F, _F, _F, _P, wap_layout_t, _P]),
     ("wap_lrn_bwd", _I, [_P, wap_layout_t, _P, wap_layout_t, _I, _F, _F, _F, _P, wap_layout_t, _P,

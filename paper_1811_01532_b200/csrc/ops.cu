@@ -343,80 +343,96 @@ __global__ void col2im_kernel(const float* __restrict__ dcol, int64_t ldcol, int
 // ---------------------------------------------------------------------------
 // MaxPool
 // ---------------------------------------------------------------------------
-__global__ void maxpool_fwd_kernel(const float* __restrict__ x, wap_layout_t xl, int win, int s,
-                                   float* __restrict__ y, wap_layout_t yl, uint8_t* __restrict__ arg) {
+// Row-blocked launches: blockIdx.y = b * H + h (one output row for the forward,
+// one input row for the backward), threads sweep (w, 4-channel group) of that row
+// with 32-bit indices; row geometry is decoded once per block.
+//
+// ReLU-fused argmax (flags & WAP_POOL_RELU_FUSED): when the pool input is a ReLU
+// output and the backward is fused with that ReLU's GradReLU, the forward stores
+// 0xFF for windows whose max is <= 0. The GradReLU mask at the argmax element is
+// exactly (max > 0) (the max of ReLU outputs is positive iff its first argmax is),
+// so the backward needs no mask read (interp.py:197-198 on the pooled element).
+constexpr uint8_t kNoGrad = 0xFF;
+
+__global__ void __launch_bounds__(256) maxpool_fwd_kernel(const float* __restrict__ x, wap_layout_t xl, int win,
+                                                          int s, float* __restrict__ y, wap_layout_t yl,
+                                                          uint8_t* __restrict__ arg, int relu_fused) {
   const int c4n = yl.ld / 4;
-  const int64_t total = (int64_t)yl.B * yl.H * yl.W * c4n;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % c4n) * 4;
-    int64_t q = i / c4n;
-    const int wo = (int)(q % yl.W);
-    q /= yl.W;
-    const int ho = (int)(q % yl.H);
-    const int b = (int)(q / yl.H);
+  const int row = blockIdx.y;
+  const int b = row / yl.H, ho = row - (row / yl.H) * yl.H;
+  const int per = yl.W * c4n;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < per; j += gridDim.x * blockDim.x) {
+    const int wo = j / c4n;
+    const int c = (j - wo * c4n) * 4;
     float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
     int bi[4] = {0, 0, 0, 0};
-    for (int a = 0; a < win; ++a)
+    const float* xr = x + lidx(xl, b, ho * s, wo * s, c);
+    const int64_t xrow = (int64_t)(xl.W + 2 * xl.pad) * xl.ld;
+    for (int a2 = 0; a2 < win; ++a2)
       for (int bb = 0; bb < win; ++bb) {
-        const float4 v = *reinterpret_cast<const float4*>(x + lidx(xl, b, ho * s + a, wo * s + bb, c));
+        const float4 v = *reinterpret_cast<const float4*>(xr + a2 * xrow + (int64_t)bb * xl.ld);
         const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (vv[j] > best[j]) { best[j] = vv[j]; bi[j] = a * win + bb; }
+        for (int t = 0; t < 4; ++t)
+          if (vv[t] > best[t]) { best[t] = vv[t]; bi[t] = a2 * win + bb; }
       }
     float o[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) o[j] = (c + j < yl.C) ? best[j] : 0.f;
+    for (int t = 0; t < 4; ++t) {
+      o[t] = (c + t < yl.C) ? best[t] : 0.f;
+      if (relu_fused && !(best[t] > 0.f)) bi[t] = kNoGrad;
+    }
     const int64_t yi = lidx(yl, b, ho, wo, c);
     *reinterpret_cast<float4*>(y + yi) = make_float4(o[0], o[1], o[2], o[3]);
-    if (arg) {
-      uchar4 a4 = make_uchar4((uint8_t)bi[0], (uint8_t)bi[1], (uint8_t)bi[2], (uint8_t)bi[3]);
-      *reinterpret_cast<uchar4*>(arg + yi) = a4;
-    }
+    if (arg) *reinterpret_cast<uchar4*>(arg + yi) = make_uchar4((uint8_t)bi[0], (uint8_t)bi[1], (uint8_t)bi[2],
+                                                                (uint8_t)bi[3]);
   }
 }
 
-__global__ void maxpool_bwd_kernel(const uint8_t* __restrict__ arg, const float* __restrict__ dy, wap_layout_t yl,
-                                   int win, int s, float* __restrict__ dx, wap_layout_t xl,
-                                   const float* __restrict__ mask, wap_layout_t ml) {
+__global__ void __launch_bounds__(256) maxpool_bwd_kernel(const uint8_t* __restrict__ arg,
+                                                          const float* __restrict__ dy, wap_layout_t yl, int win,
+                                                          int s, float* __restrict__ dx, wap_layout_t xl,
+                                                          const float* __restrict__ mask, wap_layout_t ml) {
   const int c4n = xl.ld / 4;
-  const int64_t total = (int64_t)xl.B * xl.H * xl.W * c4n;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % c4n) * 4;
-    int64_t q = i / c4n;
-    const int w = (int)(q % xl.W);
-    q /= xl.W;
-    const int h = (int)(q % xl.H);
-    const int b = (int)(q / xl.H);
+  const int row = blockIdx.y;
+  const int b = row / xl.H, h = row - (row / xl.H) * xl.H;
+  // windows (ho, wo) with ho*s <= h < ho*s + win
+  const int ho_lo = h >= win ? (h - win) / s + 1 : 0;
+  const int ho_hi = min(h / s, yl.H - 1);
+  const int per = xl.W * c4n;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < per; j += gridDim.x * blockDim.x) {
+    const int w = j / c4n;
+    const int c = (j - w * c4n) * 4;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    // windows (ho, wo) with ho*s <= h < ho*s + win
-    const int ho_lo = h >= win ? (h - win) / s + 1 : 0;
-    const int ho_hi = min(h / s, yl.H - 1);
     const int wo_lo = w >= win ? (w - win) / s + 1 : 0;
     const int wo_hi = min(w / s, yl.W - 1);
     for (int ho = ho_lo; ho <= ho_hi; ++ho)
       for (int wo = wo_lo; wo <= wo_hi; ++wo) {
         const int local = (h - ho * s) * win + (w - wo * s);
         const int64_t yi = lidx(yl, b, ho, wo, c);
-        const uchar4 a = *reinterpret_cast<const uchar4*>(arg + yi);
-        const float4 g = *reinterpret_cast<const float4*>(dy + yi);
-        if (a.x == local) acc[0] += g.x;
-        if (a.y == local) acc[1] += g.y;
-        if (a.z == local) acc[2] += g.z;
-        if (a.w == local) acc[3] += g.w;
+        const uchar4 a4 = *reinterpret_cast<const uchar4*>(arg + yi);
+        const float4 g = __ldg(reinterpret_cast<const float4*>(dy + yi));
+        if (a4.x == local) acc[0] += g.x;
+        if (a4.y == local) acc[1] += g.y;
+        if (a4.z == local) acc[2] += g.z;
+        if (a4.w == local) acc[3] += g.w;
       }
     if (mask) {
-      const float4 m = *reinterpret_cast<const float4*>(mask + lidx(ml, b, h, w, c));
+      const float4 m = __ldg(reinterpret_cast<const float4*>(mask + lidx(ml, b, h, w, c)));
       if (!(m.x > 0.f)) acc[0] = 0.f;
       if (!(m.y > 0.f)) acc[1] = 0.f;
       if (!(m.z > 0.f)) acc[2] = 0.f;
       if (!(m.w > 0.f)) acc[3] = 0.f;
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (c + j >= xl.C) acc[j] = 0.f;
+    for (int t = 0; t < 4; ++t)
+      if (c + t >= xl.C) acc[t] = 0.f;
     *reinterpret_cast<float4*>(dx + lidx(xl, b, h, w, c)) = make_float4(acc[0], acc[1], acc[2], acc[3]);
   }
+}
+
+dim3 pool_grid(int rows, int per) {
+  return dim3((unsigned)std::max(1, std::min((per + 255) / 256, 64)), (unsigned)rows);
 }
 
 // ---------------------------------------------------------------------------
@@ -930,14 +946,21 @@ extern "C" int wap_col2im(const float* dcol, int64_t ldcol, int k, int stride, i
 
 extern "C" int wap_maxpool_fwd(const float* x, wap_layout_t xl, int window, int stride, float* y, wap_layout_t yl,
                                uint8_t* argmax, void* stream) {
+  return wap_maxpool_fwd_ex(x, xl, window, stride, y, yl, argmax, 0, stream);
+}
+
+extern "C" int wap_maxpool_fwd_ex(const float* x, wap_layout_t xl, int window, int stride, float* y, wap_layout_t yl,
+                                  uint8_t* argmax, int flags, void* stream) {
   int rc;
   if ((rc = check_layout(xl, "x")) || (rc = check_layout(yl, "y"))) return rc;
   WAP_CHECK_ARG(window >= 1 && window <= 15 && stride >= 1, "maxpool: bad window/stride");
   WAP_CHECK_ARG(yl.H == (xl.H - window) / stride + 1 && yl.W == (xl.W - window) / stride + 1 && yl.C == xl.C &&
                     yl.B == xl.B && xl.ld == yl.ld,
                 "maxpool: output layout does not match");
-  const int64_t work = (int64_t)yl.B * yl.H * yl.W * (yl.ld / 4);
-  maxpool_fwd_kernel<<<grid_for(work, 256), 256, 0, STREAM(stream)>>>(x, xl, window, stride, y, yl, argmax);
+  WAP_CHECK_ARG((int64_t)yl.B * yl.H < 65536 * 1024LL, "maxpool: too many rows");
+  const int per = yl.W * (yl.ld / 4);
+  maxpool_fwd_kernel<<<pool_grid(yl.B * yl.H, per), 256, 0, STREAM(stream)>>>(
+      x, xl, window, stride, y, yl, argmax, (flags & WAP_POOL_RELU_FUSED) ? 1 : 0);
   WAP_LAUNCH_CHECK();
   COUNT_LAUNCH();
   return WAP_OK;
@@ -950,9 +973,9 @@ extern "C" int wap_maxpool_bwd(const uint8_t* argmax, const float* dy, wap_layou
   if (mask && (rc = check_layout(ml, "mask"))) return rc;
   WAP_CHECK_ARG(argmax != nullptr, "maxpool backward needs the forward argmax");
   WAP_CHECK_ARG(dxl.ld == dyl.ld, "maxpool: dx/dy ld mismatch");
-  const int64_t work = (int64_t)dxl.B * dxl.H * dxl.W * (dxl.ld / 4);
-  maxpool_bwd_kernel<<<grid_for(work, 256), 256, 0, STREAM(stream)>>>(argmax, dy, dyl, window, stride, dx, dxl, mask,
-                                                                     ml);
+  const int per = dxl.W * (dxl.ld / 4);
+  maxpool_bwd_kernel<<<pool_grid(dxl.B * dxl.H, per), 256, 0, STREAM(stream)>>>(argmax, dy, dyl, window, stride, dx,
+                                                                                 dxl, mask, ml);
   WAP_LAUNCH_CHECK();
   COUNT_LAUNCH();
   return WAP_OK;

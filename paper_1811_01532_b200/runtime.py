@@ -283,6 +283,17 @@ class Program:
             n = self.node(nid)
             if n.kind is OpKind.MAX_POOL:
                 self.pool_of[(n.inputs[0], n.attr("window"), n.attr("stride"))] = nid
+        # pools whose every backward is fused with the GradReLU of the ReLU feeding them:
+        # the argmax can carry that mask (WAP_POOL_RELU_FUSED)
+        self.pool_relu_fused: set[str] = set()
+        for key, pool in self.pool_of.items():
+            x_id = key[0]
+            grads = [u for u in self.order if self.kind(u) is OpKind.GRAD_MAX_POOL
+                     and (self.node(u).inputs[0], self.node(u).attr("window"), self.node(u).attr("stride")) == key]
+            if grads and all(g in self.bwd_mask and
+                             self.mask_src(self.node(self.bwd_mask[g]).inputs[0]) == self.mask_src(x_id)
+                             for g in grads):
+                self.pool_relu_fused.add(pool)
 
     def mask_src(self, nid: str) -> str:
         return self.mask_alias.get(nid, nid)
@@ -910,8 +921,9 @@ class Program:
             raise EvalError("MaxPool needs equal channel strides")
         arg = self.torch.zeros(y.numel_storage(), dtype=self.torch.uint8, device=self.device)
         self.t[f"{n.id}::argmax"] = Tensor(y.dims, y.pad, y.ld, arg, "nhwc")
-        self._emit(n.id, self.L.wap_maxpool_fwd,
-                   (x.ptr, x.layout(), n.attr("window"), n.attr("stride"), y.ptr, y.layout(), arg.data_ptr()),
+        flags = N.POOL_RELU_FUSED if n.id in self.pool_relu_fused else 0
+        self._emit(n.id, self.L.wap_maxpool_fwd_ex,
+                   (x.ptr, x.layout(), n.attr("window"), n.attr("stride"), y.ptr, y.layout(), arg.data_ptr(), flags),
                    "MaxPool", keep=[arg], alg_bytes=self._nbytes(x, y) + self._nbytes(y) // 4)
 
     def _lower_pool_grad(self, n: Node) -> None:
@@ -924,6 +936,8 @@ class Program:
         gr = self.bwd_mask.get(n.id)
         out = self._out(gr if gr else n.id)
         mask = self._in(self.node(gr), self.mask_src(self.node(gr).inputs[0])) if gr else None
+        if pool in self.pool_relu_fused:
+            mask = None  # the forward argmax already encodes the GradReLU mask
         ml = mask.layout() if mask is not None else N.wap_layout_t()
         if dy.pad != arg.pad:
             raise EvalError("MaxPool gradient must share the pooled output layout")
