@@ -441,10 +441,13 @@ dim3 pool_grid(int rows, int per) {
 constexpr int LRN_PIX = 8;
 
 __device__ __forceinline__ void pixel_of(const wap_layout_t& l, int64_t p, int& b, int& h, int& w) {
-  w = (int)(p % l.W);
-  p /= l.W;
-  h = (int)(p % l.H);
-  b = (int)(p / l.H);
+  // pixel counts of one layer stay below 2^31 (host-checked): 32-bit division
+  const uint32_t q = (uint32_t)p;
+  const uint32_t r = q / (uint32_t)l.W;
+  w = (int)(q - r * (uint32_t)l.W);
+  const uint32_t bb = r / (uint32_t)l.H;
+  h = (int)(r - bb * (uint32_t)l.H);
+  b = (int)bb;
 }
 
 __global__ void lrn_fwd_kernel(const float* __restrict__ x, wap_layout_t xl, int size, float alpha, float beta,
@@ -638,6 +641,7 @@ __global__ void __launch_bounds__(256) lrn_warp_kernel(const float* __restrict__
   constexpr int NV = 4 * VPL;
   const int lane = threadIdx.x & 31;
   const int sl = lane & 15;
+  const bool mask_is_x = BWD && mask == x && ml.pad == xl.pad && ml.ld == xl.ld;
   const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -683,7 +687,7 @@ __global__ void __launch_bounds__(256) lrn_warp_kernel(const float* __restrict__
     } else {
       float t[NV];
 #pragma unroll
-      for (int j = 0; j < NV; ++j) t[j] = d[j] * v[j] * pw[j] / s[j];
+      for (int j = 0; j < NV; ++j) t[j] = __fdividef(d[j] * v[j] * pw[j], s[j]);
       float tm2 = __shfl_up_sync(0xffffffffu, t[NV - 2], 1, 16), tm1 = __shfl_up_sync(0xffffffffu, t[NV - 1], 1, 16);
       float tp0 = __shfl_down_sync(0xffffffffu, t[0], 1, 16), tp1 = __shfl_down_sync(0xffffffffu, t[1], 1, 16);
       if (sl == 0) tm2 = tm1 = 0.f;
@@ -702,7 +706,13 @@ __global__ void __launch_bounds__(256) lrn_warp_kernel(const float* __restrict__
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       float4 r = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
-      if (BWD && mask) {
+      if (BWD && mask_is_x) {
+        // GradReLU mask source is the LRN input itself (ReLU -> LRN): reuse the loaded x
+        if (!(v[4 * i] > 0.f)) r.x = 0.f;
+        if (!(v[4 * i + 1] > 0.f)) r.y = 0.f;
+        if (!(v[4 * i + 2] > 0.f)) r.z = 0.f;
+        if (!(v[4 * i + 3] > 0.f)) r.w = 0.f;
+      } else if (BWD && mask) {
         const float4 m = *reinterpret_cast<const float4*>(mask + lidx(ml, b, h, w, c0 + 4 * i));
         if (!(m.x > 0.f)) r.x = 0.f;
         if (!(m.y > 0.f)) r.y = 0.f;
@@ -987,6 +997,7 @@ extern "C" int wap_lrn_fwd(const float* x, wap_layout_t xl, int size, float alph
   if ((rc = check_layout(xl, "x")) || (rc = check_layout(yl, "y"))) return rc;
   WAP_CHECK_ARG(size >= 1 && size % 2 == 1, "LRN size must be odd");
   const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
+  WAP_CHECK_ARG(npix < (1LL << 31), "LRN: pixel count must stay below 2^31");
   const int smem = LRN_PIX * xl.C * 4;
   if (!launch_lrn_fast<false>(x, xl, nullptr, xl, size, alpha, beta, bias, y, yl, nullptr, xl, STREAM(stream)))
     lrn_fwd_kernel<<<grid_for(npix, LRN_PIX), 256, smem, STREAM(stream)>>>(x, xl, size, alpha, beta, bias, y, yl);
@@ -1002,6 +1013,7 @@ extern "C" int wap_lrn_bwd(const float* x, wap_layout_t xl, const float* dy, wap
   if ((rc = check_layout(xl, "x")) || (rc = check_layout(dyl, "dy")) || (rc = check_layout(dxl, "dx"))) return rc;
   if (mask && (rc = check_layout(ml, "mask"))) return rc;
   const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
+  WAP_CHECK_ARG(npix < (1LL << 31), "LRN: pixel count must stay below 2^31");
   const int smem = 4 * LRN_PIX * xl.C * 4;
   if (!launch_lrn_fast<true>(x, xl, dy, dyl, size, alpha, beta, bias, dx, dxl, mask, ml, STREAM(stream)))
     lrn_bwd_kernel<<<grid_for(npix, LRN_PIX), 256, smem, STREAM(stream)>>>(x, xl, dy, dyl, size, alpha, beta, bias,

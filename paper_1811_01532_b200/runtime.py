@@ -965,7 +965,8 @@ class Program:
         self._emit(n.id, self.L.wap_lrn_bwd,
                    (x.ptr, x.layout(), dy.ptr, dy.layout(), a["size"], C.c_float(a["alpha"]), C.c_float(a["beta"]),
                     C.c_float(a["bias"]), out.ptr, out.layout(), mask.ptr if mask is not None else None, ml),
-                   "GradLRN", alg_bytes=self._nbytes(x, dy, out, mask))
+                   "GradLRN", alg_bytes=self._nbytes(x, dy, out) + (0 if mask is None or mask.ptr == x.ptr
+                                                                     else self._nbytes(mask)))
 
     # -- aggregation / update ------------------------------------------------
     def _lower_add_n(self, n: Node) -> None:
