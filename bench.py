@@ -214,6 +214,7 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(reps):
         evs = []
         for st in prog.steps:
+            st = getattr(st, "inner", st)  # parallel-stream steps are timed on this stream
             a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             st(N.stream_ptr())

@@ -506,10 +506,32 @@ class Program:
             self.step_end[nid] = len(self.steps)
         if self.autotune:
             self._autotune_gemms()
+        self._parallelize_weight_grads()
         self._schedule_collectives()
         self._fuse_updates()
         self.steps.extend(self.update_steps)
         self.update_steps = []
+
+    def _parallelize_weight_grads(self) -> None:
+        """Training (in-place) programs: weight and bias gradients (GradConv2DW,
+        GradMatMulW, GradBias) depend only on forward activations and the layer's
+        upstream gradient, and feed only the update / allreduce. Issue them on a
+        second stream forked at their position, so they overlap the data-gradient
+        chain (dgrad of the same layer and everything below it); a join before the
+        updates restores the order. Captured CUDA graphs keep the two branches."""
+        self.par_stream = None
+        if not self.in_place:
+            return
+        kinds = (OpKind.GRAD_CONV2D_W, OpKind.GRAD_MATMUL_W, OpKind.GRAD_BIAS)
+        side = None
+        for i, st in enumerate(self.steps):
+            if st.name in self.g.nodes and self.kind(st.name) in kinds:
+                if side is None:
+                    side = self.torch.cuda.Stream(device=self.device)
+                self.steps[i] = _ParallelStep(st, side, self.torch)
+        if side is not None:
+            self.par_stream = side
+            self.steps.append(_JoinParallel(side, self.torch))
 
     def _lower_node(self, nid: str) -> None:
         """Lower one graph node to its launch step(s)."""
@@ -645,7 +667,7 @@ class Program:
         for ready, lo, hi, ids in buckets:
             buf = self.grad_arena[lo:hi]
             inserts.setdefault(ready, []).append(
-                _BucketStep("+".join(ids), self.collective, buf, side, self.torch))
+                _BucketStep("+".join(ids), self.collective, buf, side, self.torch, self.par_stream))
             if self.bucket_sgd:
                 vars_in = [v for o, v in var_of_slot.items() if lo <= o < hi]
                 readers = [self.step_end[u] for v in vars_in for u in self.users[v]
@@ -1031,10 +1053,18 @@ class Program:
             raise EvalError("steps with cross-process collectives are not captured")
         side = torch.cuda.Stream(device=self.device)
         side.wait_stream(torch.cuda.current_stream(self.device))
+        # the warm-up pass is a real training step (in-place SGD): keep the variables
+        # as they were, so capture() + the first replay is exactly one step
+        saved = self.var_arena.clone() if self.in_place else None
         with torch.cuda.stream(side):
             for st in self.steps:  # warm-up on the capture stream
                 st(N.stream_ptr(side))
         torch.cuda.current_stream(self.device).wait_stream(side)
+        if saved is not None:
+            torch.cuda.current_stream(self.device).synchronize()
+            self.var_arena.copy_(saved)
+            torch.cuda.current_stream(self.device).synchronize()
+            del saved
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=side):
             for st in self.steps:
@@ -1116,20 +1146,56 @@ class _CollectiveStep:
 
 
 class _BucketStep(_CollectiveStep):
-    def __init__(self, name, fn, buf, side, torch):
+    def __init__(self, name, fn, buf, side, torch, par=None):
         self.name = name
         self.fn = fn
         self.buf = buf
         self.side = side
         self.torch = torch
+        self.par = par  # stream producing weight gradients (may hold this bucket's grads)
 
     def __call__(self, stream: int) -> None:
         torch = self.torch
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream())
         self.side.wait_event(ev)
+        if self.par is not None:
+            self.side.wait_stream(self.par)
         with torch.cuda.stream(self.side):
             self.fn(self.buf)
+
+
+class _ParallelStep:
+    """A native step issued on the weight-gradient stream, forked from the current
+    stream at this point (capturable: the fork is an event wait)."""
+
+    def __init__(self, step, side, torch):
+        self.inner = step
+        self.name = step.name
+        self.side = side
+        self.torch = torch
+        for a in ("alg_flops", "alg_bytes", "shape", "desc", "call"):
+            if hasattr(step, a):
+                setattr(self, a, getattr(step, a))
+
+    def __call__(self, stream: int) -> None:
+        torch = self.torch
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.side.wait_event(ev)
+        from . import _native as N
+
+        self.inner(N.stream_ptr(self.side))
+
+
+class _JoinParallel:
+    def __init__(self, side, torch):
+        self.name = "join(wgrad)"
+        self.side = side
+        self.torch = torch
+
+    def __call__(self, stream: int) -> None:
+        self.torch.cuda.current_stream().wait_stream(self.side)
 
 
 class _SideStep(_CollectiveStep):

@@ -35,6 +35,7 @@ def main():
     s = N.stream_ptr()
     rows = []
     for st in tr.prog.steps:
+        st = getattr(st, "inner", st)
         if not isinstance(st, _GemmStep):
             continue
         st(s)

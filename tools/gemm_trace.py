@@ -29,7 +29,7 @@ def main():
     tp = trainer.plan_training(g, 1, planner.load_profile("b200"), force_d=1)
     tr = trainer.Trainer(tp, precision=args.precision, use_graph=False, variables=he_init(g))
     tr.load(synthetic_batch(g, 0, args.batch))
-    sel = [s for s in tr.prog.steps if s.name == args.only]
+    sel = [getattr(s, "inner", s) for s in tr.prog.steps if s.name == args.only]
     for _ in range(2):
         for s in sel:
             s(N.stream_ptr())

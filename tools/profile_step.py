@@ -33,7 +33,8 @@ def main():
         tr.run()
     torch.cuda.synchronize()
     names = args.only.split(",")
-    sel = [s for s in tr.prog.steps if s.name in names] or [s for s in tr.prog.steps if args.only in s.name]
+    steps = [getattr(s, "inner", s) for s in tr.prog.steps]
+    sel = [s for s in steps if s.name in names] or [s for s in steps if args.only in s.name]
     print("selected:", [s.name for s in sel], flush=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # ncu --profile-from-start off captures only this region (autotuning and
