@@ -84,10 +84,15 @@ int wap_gemm_plan_run(void* plan, void* stream);
 void wap_gemm_plan_destroy(void* plan);
 
 /* ---- activation layout --------------------------------------------------- */
-/* Logical NHWC [B, H, W, C] stored as [B, H+2*pad, W+2*pad, ld] (ld >= C,
- * ld % 4 == 0, halo rows zero). A 2D matrix [rows, cols] is B=rows, H=W=1,
- * C=cols, pad=0. Element (b,h,w,c) lives at
- *   ((b*(H+2p) + h+p)*(W+2p) + w+p)*ld + c. */
+/* Logical NHWC [B, H, W, C] stored as [B, H+pad, W+pad, ld] (ld >= C,
+ * ld % 4 == 0): each image row is followed by `pad` zero columns and each image
+ * by `pad` zero rows. Viewed as a flat [rows, ld] matrix, a filter tap (u, v) of
+ * a k x k "same" conv (k/2 <= pad) is the row shift (u-k/2)*(W+pad) + (v-k/2):
+ * left/up neighbours of the first column/row land in the previous row's or
+ * image's trailing zeros (or before the buffer: TMA OOB zero fill), so one
+ * trailing halo serves both sides. A 2D matrix [rows, cols] is B=rows,
+ * H=W=1, C=cols, pad=0. Element (b,h,w,c) lives at
+ *   ((b*(H+p) + h)*(W+p) + w)*ld + c. */
 typedef struct {
   int32_t B, H, W, C;
   int32_t pad;
@@ -96,8 +101,8 @@ typedef struct {
 
 /* im2col for Conv2D with any stride/padding (interp.py:69-79 generalised):
  * col[(b,ho,wo), (u,v,c)] = x[b, ho*s+u-p, wo*s+v-p, c] (0 outside), columns
- * K..ldcol-1 zeroed. Rows enumerate the output grid padded by out_pad (halo
- * rows zero): col is [B*(Ho+2*out_pad)*(Wo+2*out_pad), ldcol]. */
+ * K..ldcol-1 zeroed. Rows enumerate the output grid with out_pad trailing halo
+ * columns/rows (halo rows zero): col is [B*(Ho+out_pad)*(Wo+out_pad), ldcol]. */
 int wap_im2col(const float* x, wap_layout_t xl, int k, int stride, int padding, int Ho, int Wo, int out_pad,
                float* col, int64_t ldcol, void* stream);
 /* col2im (gather form, deterministic) for GradConv2DX (interp.py:94-102):

@@ -32,11 +32,15 @@ namespace wapgemm {
 
 constexpr int BM = 128;  // rows per CTA
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row
-constexpr int kSmemBudget = 204 * 1024;  // + 16.5 KB epilogue staging below
+#ifndef WAP_EPI_BUFS
+#define WAP_EPI_BUFS 1  // epilogue staging blocks per warp (2: a chunk's TMA store overlaps the next chunk)
+#endif
+constexpr int kEpiBufs = WAP_EPI_BUFS;
+constexpr int kSmemBudget = (220 - 16 * kEpiBufs) * 1024;  // + the epilogue staging below
 // epilogue staging: per warp one [32 rows][32 fp32] block in the SWIZZLE_128B
 // layout (16-byte chunk j of row r at chunk j ^ (r & 7)): conflict-free for the
 // row-per-thread writes and the coalesced reads, and the TMA store's source format
-constexpr int kEpiStage = 4 * 32 * 128;
+constexpr int kEpiStage = kEpiBufs * 4 * 32 * 128;
 constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap offsets of A, B [512,768)
 // fewest TMEM A slots (3xTF32) worth keeping two accumulators for
 #ifndef WAP_MIN_A_SLOTS
@@ -311,16 +315,19 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read_all() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+__device__ __forceinline__ void bulk_wait_read_1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ bool halo_row(const GemmArgs& g, int64_t m) {
   if (g.halo_pad <= 0) return false;
-  const int hp = g.halo_h + 2 * g.halo_pad, wp = g.halo_w + 2 * g.halo_pad;
+  const int hp = g.halo_h + g.halo_pad, wp = g.halo_w + g.halo_pad;
   // padded-grid rows of one launch stay below 2^31 (host-checked), so 32-bit math
   const int mi = (int)m;
   const int w = mi % wp;
   const int h = (mi / wp) % hp;
-  return w < g.halo_pad || w >= g.halo_pad + g.halo_w || h < g.halo_pad || h >= g.halo_pad + g.halo_h;
+  return w >= g.halo_w || h >= g.halo_h;  // trailing halo columns / rows of each image
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -705,7 +712,9 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
     // together; the result goes back to the block and leaves through one TMA
     // bulk tensor store (split-K partial slabs: direct 16-byte stores).
     const int wq = warp - 4;  // TMEM lane quarter
-    const uint32_t stg_s = smem_u32(epi_base) + wq * (32 * 128);
+    const uint32_t stg_base = smem_u32(epi_base) + wq * (32 * 128);
+    uint32_t stg_s = stg_base;
+    int ebuf = 0;  // staging block of the current chunk (kEpiBufs-deep ring)
     // 16-byte chunk q of staged row r (SWIZZLE_128B)
     auto stg_at = [&](int r, int q) { return stg_s + (uint32_t)(r * 128 + ((q ^ (r & 7)) << 4)); };
     const uint32_t tempty_leader = CG == 2 ? map_to_rank(smem_u32(&tempty_bar[0]), 0) : smem_u32(&tempty_bar[0]);
@@ -774,7 +783,15 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         const int col = nb + c4;
         // 1) raw accumulator row -> smem block
         // the TMA store of the previous chunk must have read the staging block
-        if (tma_out) bulk_wait_read_all();
+        if (kEpiBufs > 1) {
+          stg_s = stg_base + (uint32_t)(ebuf * 4 * 32 * 128);
+          ebuf = ebuf + 1 == kEpiBufs ? 0 : ebuf + 1;
+        }
+        // the TMA store that last used this staging block must have read it
+        if (tma_out) {
+          if (kEpiBufs > 1) bulk_wait_read_1();
+          else bulk_wait_read_all();
+        }
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 32; j += 4) st_shared_v4(stg_at(lane, j >> 2), v[j], v[j + 1], v[j + 2], v[j + 3]);

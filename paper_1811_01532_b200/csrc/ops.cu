@@ -13,7 +13,7 @@ extern std::atomic<long long> g_wap_launches;
 namespace {
 
 __host__ __device__ __forceinline__ int64_t lidx(const wap_layout_t& l, int b, int h, int w, int c) {
-  return (((int64_t)b * (l.H + 2 * l.pad) + h + l.pad) * (l.W + 2 * l.pad) + w + l.pad) * l.ld + c;
+  return (((int64_t)b * (l.H + l.pad) + h) * (l.W + l.pad) + w) * l.ld + c;
 }
 
 int grid_for(int64_t work, int threads) {
@@ -150,7 +150,7 @@ __global__ void bias_grad_final(const float* __restrict__ part, int chunks, int 
 }
 
 int bias_chunks(const wap_layout_t& l) {
-  const int64_t rows = (int64_t)l.B * (l.H + 2 * l.pad) * (l.W + 2 * l.pad);
+  const int64_t rows = (int64_t)l.B * (l.H + l.pad) * (l.W + l.pad);
   const int cw = bias_cw(l);
   const int ctiles = (l.ld / 4 + cw - 1) / cw;
   // enough blocks (8 per SM) to keep ~64 KB of loads in flight per SM
@@ -164,13 +164,14 @@ int bias_chunks(const wap_layout_t& l) {
 // ---------------------------------------------------------------------------
 // im2col / col2im
 // ---------------------------------------------------------------------------
-// Rows of `col` enumerate the OUTPUT grid padded by P (halo rows are zero), so a
-// conv whose output must live on a padded grid gets GEMM rows that line up with it.
+// Rows of `col` enumerate the OUTPUT grid with P trailing halo columns / rows per
+// image (halo rows are zero), so a conv whose output must live on a padded grid
+// gets GEMM rows that line up with it.
 __global__ void im2col_kernel(const float* __restrict__ x, wap_layout_t xl, int k, int s, int p, int Ho, int Wo,
                               int P, float* __restrict__ col, int64_t ldcol) {
   const int C = xl.C;
   const int K = k * k * C;
-  const int Hp = Ho + 2 * P, Wp = Wo + 2 * P;
+  const int Hp = Ho + P, Wp = Wo + P;
   const int64_t M = (int64_t)xl.B * Hp * Wp;
   const int64_t total = M * ldcol;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -181,9 +182,9 @@ __global__ void im2col_kernel(const float* __restrict__ x, wap_layout_t xl, int 
       const int c = kk % C;
       const int t = kk / C;
       const int u = t / k, vv = t % k;
-      const int wo = (int)(m % Wp) - P;
+      const int wo = (int)(m % Wp);
       const int64_t r = m / Wp;
-      const int ho = (int)(r % Hp) - P;
+      const int ho = (int)(r % Hp);
       const int b = (int)(r / Hp);
       const int hi = ho * s + u - p, wi = wo * s + vv - p;
       if (ho >= 0 && ho < Ho && wo >= 0 && wo < Wo && hi >= 0 && hi < xl.H && wi >= 0 && wi < xl.W)
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(256) im2col_table_kernel(const float* __restri
   __shared__ int64_t rbase[IM2COL_ROWS];
   const int C = xl.C;
   const int K = k * k * C;
-  const int Wxp = xl.W + 2 * xl.pad;
+  const int Wxp = xl.W + xl.pad;
   for (int kk = threadIdx.x; kk < K; kk += blockDim.x) {
     const int c = kk % C, t = kk / C;
     const int u = t / k, v = t % k;
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(256) im2col_table_kernel(const float* __restri
     tv[kk] = (short)v;
     toff[kk] = (u * Wxp + v) * xl.ld + c;
   }
-  const int Hp = Ho + 2 * P, Wp = Wo + 2 * P;
+  const int Hp = Ho + P, Wp = Wo + P;
   __syncthreads();
   if (ldcol % 4 == 0) {
     // float4 path: a block sweeps IM2COL_ROWS rows at a time; row geometry comes
@@ -230,14 +231,14 @@ __global__ void __launch_bounds__(256) im2col_table_kernel(const float* __restri
         int64_t base = 0;  // may be negative: taps outside the image are masked per element
         int h0 = 0, w0 = 0, valid = 0;
         if (m < M) {
-          const int wo = (int)(m % Wp) - P;
+          const int wo = (int)(m % Wp);
           const int64_t q = m / Wp;
-          const int ho = (int)(q % Hp) - P;
+          const int ho = (int)(q % Hp);
           const int bb = (int)(q / Hp);
           if (ho >= 0 && ho < Ho && wo >= 0 && wo < Wo) {
             h0 = ho * s - p;
             w0 = wo * s - p;
-            base = (((int64_t)bb * (xl.H + 2 * xl.pad) + h0 + xl.pad) * Wxp + w0 + xl.pad) * xl.ld;
+            base = (((int64_t)bb * (xl.H + xl.pad) + h0) * Wxp + w0) * xl.ld;
             valid = 1;
           }
         }
@@ -276,9 +277,9 @@ __global__ void __launch_bounds__(256) im2col_table_kernel(const float* __restri
       const int64_t m = r0 + threadIdx.x;
       int b = -1, ho = -1, wo = -1;
       if (m < M) {
-        wo = (int)(m % Wp) - P;
+        wo = (int)(m % Wp);
         const int64_t q = m / Wp;
-        ho = (int)(q % Hp) - P;
+        ho = (int)(q % Hp);
         b = (int)(q / Hp);
         if (ho < 0 || ho >= Ho || wo < 0 || wo >= Wo) b = -2;  // halo row -> zeros
       }
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(256) im2col_table_kernel(const float* __restri
       const int b = rb[i], h0 = rh[i], w0 = rw[i];
       float* out = col + m * ldcol;
       // base address of tap (0,0) channel 0 (may be outside; guarded per element)
-      const int64_t base = (((int64_t)(b < 0 ? 0 : b) * (xl.H + 2 * xl.pad) + h0 + xl.pad) * Wxp + w0 + xl.pad) * xl.ld;
+      const int64_t base = (((int64_t)(b < 0 ? 0 : b) * (xl.H + xl.pad) + h0) * Wxp + w0) * xl.ld;
       for (int kk = threadIdx.x; kk < ldcol; kk += blockDim.x) {
         float v = 0.f;
         if (b >= 0 && kk < K) {
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(256) im2col_table_kernel(const float* __restri
 __global__ void col2im_kernel(const float* __restrict__ dcol, int64_t ldcol, int k, int s, int p, int Ho, int Wo,
                               int P, float* __restrict__ dx, wap_layout_t dl, const float* __restrict__ mask,
                               wap_layout_t ml) {
-  const int Hp = Ho + 2 * P, Wp = Wo + 2 * P;
+  const int Hp = Ho + P, Wp = Wo + P;
   const int C = dl.C;
   const int64_t total = (int64_t)dl.B * dl.H * dl.W * dl.ld;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -331,7 +332,7 @@ __global__ void col2im_kernel(const float* __restrict__ dcol, int64_t ldcol, int
           if (ws < 0 || ws % s) continue;
           const int wo = ws / s;
           if (wo >= Wo) continue;
-          acc += dcol[(((int64_t)b * Hp + ho + P) * Wp + wo + P) * ldcol + (u * k + v) * C + c];
+          acc += dcol[(((int64_t)b * Hp + ho) * Wp + wo) * ldcol + (u * k + v) * C + c];
         }
       }
       if (mask && !(mask[lidx(ml, b, h, w, c)] > 0.f)) acc = 0.f;
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(256) maxpool_fwd_kernel(const float* __restric
     float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
     int bi[4] = {0, 0, 0, 0};
     const float* xr = x + lidx(xl, b, ho * s, wo * s, c);
-    const int64_t xrow = (int64_t)(xl.W + 2 * xl.pad) * xl.ld;
+    const int64_t xrow = (int64_t)(xl.W + xl.pad) * xl.ld;
     for (int a2 = 0; a2 < win; ++a2)
       for (int bb = 0; bb < win; ++bb) {
         const float4 v = *reinterpret_cast<const float4*>(xr + a2 * xrow + (int64_t)bb * xl.ld);
@@ -891,7 +892,7 @@ extern "C" int wap_add_n(const float* const* xs, int n, wap_layout_t l, float* y
     WAP_CHECK_ARG(xs[i] != nullptr, "null operand %d", i);
     pk.p[i] = xs[i];
   }
-  const int64_t n4 = (int64_t)l.B * (l.H + 2 * l.pad) * (l.W + 2 * l.pad) * l.ld / 4;
+  const int64_t n4 = (int64_t)l.B * (l.H + l.pad) * (l.W + l.pad) * l.ld / 4;
   add_n_kernel_packed<<<grid_for(n4, 256), 256, 0, STREAM(stream)>>>(pk, n, y, n4);
   WAP_LAUNCH_CHECK();
   COUNT_LAUNCH();
@@ -904,7 +905,7 @@ extern "C" int wap_bias_grad(const float* dy, wap_layout_t l, float* db, float* 
   int rc;
   if ((rc = check_layout(l, "dy"))) return rc;
   WAP_CHECK_ARG(dy && db && work, "null pointer");
-  const int64_t rows = (int64_t)l.B * (l.H + 2 * l.pad) * (l.W + 2 * l.pad);
+  const int64_t rows = (int64_t)l.B * (l.H + l.pad) * (l.W + l.pad);
   const int chunks = bias_chunks(l);
   const int64_t rpc = (rows + chunks - 1) / chunks;
   const int cw = bias_cw(l);
@@ -923,7 +924,7 @@ extern "C" int wap_im2col(const float* x, wap_layout_t xl, int k, int stride, in
   if ((rc = check_layout(xl, "x"))) return rc;
   WAP_CHECK_ARG(k >= 1 && stride >= 1 && padding >= 0 && Ho >= 1 && Wo >= 1 && out_pad >= 0, "im2col: bad geometry");
   WAP_CHECK_ARG(ldcol >= (int64_t)k * k * xl.C, "im2col: ldcol too small");
-  const int64_t M = (int64_t)xl.B * (Ho + 2 * out_pad) * (Wo + 2 * out_pad);
+  const int64_t M = (int64_t)xl.B * (Ho + out_pad) * (Wo + out_pad);
   const int64_t total = M * ldcol;
   if ((int64_t)k * k * xl.C <= IM2COL_MAXK) {
     int64_t blocks = (M + IM2COL_ROWS - 1) / IM2COL_ROWS;

@@ -6,11 +6,13 @@ through `_native`; nothing falls back to torch math.
 
 Padded-flat NHWC layout (the layout every stride-1 convolution runs in):
 an activation of logical shape [B, H, W, C] with halo p is stored as
-[B, H+2p, W+2p, C], halo rows zero. Viewed as a matrix [B*(H+2p)*(W+2p), C],
-filter tap (u, v) of a same-padded KxK conv is a constant row shift
-(u-p)*(W+2p) + (v-p), so Conv2D / GradConv2DX / GradConv2DW
-(interp.py:69-102) become shifted GEMMs fed by 2D TMA; out-of-range rows read
-as zero via the TMA OOB fill.
+[B, H+p, W+p, C]: p trailing zero columns after every image row and p zero
+rows after every image. Viewed as a matrix [B*(H+p)*(W+p), C], filter tap
+(u, v) of a same-padded KxK conv (K//2 <= p) is a constant row shift
+(u-K//2)*(W+p) + (v-K//2); neighbours left of column 0 / above row 0 land in the
+previous row's / image's trailing zeros, or before the buffer where the TMA
+OOB fill reads zero. So Conv2D / GradConv2DX / GradConv2DW (interp.py:69-102)
+become shifted GEMMs fed by 2D TMA with one trailing halo instead of two.
 """
 
 from __future__ import annotations
@@ -97,8 +99,9 @@ def conv_fprop(xp, w, y, *, B, H, W, Ci, Co, k, pad, bias=None, relu=False, prec
                run=True, stream=None):
     """y_pad = conv(x_pad, w) (+bias, ReLU) on the padded-flat grid; halo rows written 0.
 
-    xp: [B, H+2p, W+2p, Ci]; w: [k, k, Ci, Co] (KKIO); y: [B, H+2p, W+2p, Co]."""
-    hp, wp = H + 2 * pad, W + 2 * pad
+    xp: [B, H+p, W+p, Ci] (p trailing zero columns / rows); w: [k, k, Ci, Co] (KKIO);
+    y: [B, H+p, W+p, Co]."""
+    hp, wp = H + pad, W + pad
     rows = B * hp * wp
     ao = N.operand(xp, inner=Ci, outer=rows, ld=Ci, mn_major=False, tap_period=Ci,
                    offsets=tuple(tap_shifts(k, pad, wp)))
@@ -114,7 +117,7 @@ def conv_fprop(xp, w, y, *, B, H, W, Ci, Co, k, pad, bias=None, relu=False, prec
 def conv_dgrad(dyp, w, dxp, *, B, H, W, Ci, Co, k, pad, mask=None, precision=3, run=True,
                stream=None):
     """dx_pad = GradConv2DX(dy_pad, w) (* [mask > 0]); dy halo must be zero."""
-    hp, wp = H + 2 * pad, W + 2 * pad
+    hp, wp = H + pad, W + pad
     rows = B * hp * wp
     shifts = tap_shifts(k, pad, wp)
     ao = N.operand(dyp, inner=Co, outer=rows, ld=Co, mn_major=False, tap_period=Co,
@@ -132,7 +135,7 @@ def conv_dgrad(dyp, w, dxp, *, B, H, W, Ci, Co, k, pad, mask=None, precision=3, 
 def conv_wgrad(xp, dyp, dw, *, B, H, W, Ci, Co, k, pad, precision=3, splits=0, run=True,
                stream=None):
     """dw[k,k,Ci,Co] = GradConv2DW(x_pad, dy_pad); dy halo must be zero."""
-    hp, wp = H + 2 * pad, W + 2 * pad
+    hp, wp = H + pad, W + pad
     rows = B * hp * wp
     ao = N.operand(xp, inner=Ci, outer=rows, ld=Ci, mn_major=True, tap_period=Ci,
                    offsets=tuple(tap_shifts(k, pad, wp)))

@@ -14,8 +14,8 @@ This is the B200 replacement of the reference's per-OpKind interpreter loop
    ReLU in the GEMM epilogue, GradReLU into the producer of its upstream
    gradient (dgrad / FC-dX epilogue, MaxPool/LRN backward, col2im),
    SoftmaxXentLoss + GradSoftmaxXent in one kernel;
-3. assigns every tensor a layout (NHWC with a zero halo of `pad` pixels and a
-   channel stride `ld` rounded to 4) by solving "same grid" constraints with a
+3. assigns every tensor a layout (NHWC with `pad` trailing zero columns per
+   image row and zero rows per image, and a channel stride `ld` rounded to 4) by solving "same grid" constraints with a
    union-find, so a conv's input, output, gradients and weight-gradient
    operands share one padded-flat grid;
 4. allocates all buffers once (variables and their gradients in two flat
@@ -99,7 +99,7 @@ class Tensor:
         """Rows of the 2D [rows, ld] view (padded grid rows for NHWC)."""
         if self.kind == "nhwc":
             b, h, w, _ = self.dims
-            return b * (h + 2 * self.pad) * (w + 2 * self.pad)
+            return b * (h + self.pad) * (w + self.pad)
         if self.kind == "mat":
             return self.dims[0]
         if self.kind == "kkio":
@@ -751,7 +751,7 @@ class Program:
         if self.strategy[n.id] == "shifted":
             P = x.pad
             assert y.pad == P, (n.id, y.pad, P)
-            wp = x.dims[2] + 2 * P
+            wp = x.dims[2] + P
             shifts = [(u - p) * wp + (v - p) for u in range(kk) for v in range(kk)]
             a = self._operand(x, False, inner=ci, tap_period=ci, offsets=tuple(shifts))
             bo = N.operand(w.ptr, inner=co, outer=kk * kk * ci, ld=w.ld, mn_major=True)
@@ -760,7 +760,7 @@ class Program:
             P = y.pad
             K = kk * kk * ci
             ldcol = _ceil4(K)
-            rows = b * (ho + 2 * P) * (wo + 2 * P)
+            rows = b * (ho + P) * (wo + P)
             col = self.torch.empty(rows * ldcol, dtype=self.torch.float32, device=self.device)
             self.t[f"{n.id}::col"] = Tensor((rows, K), 0, ldcol, col, "mat")
             self._emit(n.id + "/im2col", self.L.wap_im2col,
@@ -889,7 +889,7 @@ class Program:
         if self.strategy[conv] == "shifted":
             P = dy.pad
             assert out.pad == P and (mask is None or (mask.pad == P and mask.ld == out.ld))
-            wp = out.dims[2] + 2 * P
+            wp = out.dims[2] + P
             shifts = [(u - p) * wp + (v - p) for u in range(kk) for v in range(kk)]
             a = self._operand(dy, False, inner=co, tap_period=co, offsets=tuple(-s_ for s_ in shifts))
             bo = N.operand(w.ptr, inner=co, outer=kk * kk * ci, ld=w.ld, mn_major=False, tap_period=co,
@@ -921,7 +921,7 @@ class Program:
             P = x.pad
             assert dy.pad == P
             p = kk // 2
-            wp = x.dims[2] + 2 * P
+            wp = x.dims[2] + P
             shifts = [(u - p) * wp + (v - p) for u in range(kk) for v in range(kk)]
             a = N.operand(x.ptr, inner=ci, outer=x.rows, ld=x.ld, mn_major=True, tap_period=ci,
                           offsets=tuple(shifts))
