@@ -347,6 +347,10 @@ def run_reference(args, rank, world):
 
 
 def main():
+    import faulthandler
+
+    # a stuck run leaves evidence: every thread's stack on stderr after 10 minutes
+    faulthandler.dump_traceback_later(600, exit=False)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)

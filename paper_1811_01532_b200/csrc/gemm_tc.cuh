@@ -1053,6 +1053,7 @@ struct Plan {
 };
 
 constexpr int kMaxDynSmem = 227 * 1024;
+constexpr int kExclusiveSmem = 120 * 1024;  // > half of the 228 KB per SM: one GEMM CTA per SM
 
 // dynamic shared memory of one launch (WIN adds the two A halo windows)
 template <int BN, int PREC, int CG, bool WIN>
@@ -1077,7 +1078,12 @@ int launch(const Plan& p, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.grid);
   cfg.blockDim = dim3(C::THREADS);
-  cfg.dynamicSmemBytes = smem;
+  // Every GEMM CTA claims more than half of an SM's shared memory, so two GEMM CTAs
+  // (e.g. a dgrad and a wgrad on parallel streams) never share an SM. Each holds
+  // all 512 TMEM columns (3xTF32) and a CTA pair syncs right after allocating:
+  // co-resident pairs of two kernels could otherwise each hold one SM's TMEM while
+  // waiting for their peer on the other SM (deadlock).
+  cfg.dynamicSmemBytes = smem > kExclusiveSmem ? smem : kExclusiveSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   int na = 0;
