@@ -62,17 +62,24 @@ def traffic_of(model: str, step: str):
 
 
 class ClockSampler:
-    """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
+    """nvidia-smi sampling of SM clocks / throttle reasons around the timed region.
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Sampling starts before the warm-up (nvidia-smi can take seconds to attach on a
+    fresh box) and samples are kept by their own timestamps when they fall inside
+    the timed region (else every sample of the run is reported). Stopping never
+    blocks: a sampler that does not exit after SIGTERM/SIGKILL is abandoned."""
+
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
+        self.lines: list[str] = []
+        self.window = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -81,35 +88,55 @@ class ClockSampler:
             self.proc = None
         return self
 
-    def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
+    def mark(self, t0: float, t1: float) -> None:
+        self.window = (t0, t1)
+
+    def stop(self) -> None:
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        out = ""
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
             try:
                 out, _ = self.proc.communicate(timeout=5)
             except subprocess.TimeoutExpired:
-                self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [l for l in out.splitlines() if l.strip()]
-        else:
-            self.lines = []
+                out = ""
+        self.lines = [l for l in (out or "").splitlines() if l.strip()]
+
+    @staticmethod
+    def _stamp(ts: str):
+        import datetime
+
+        try:
+            return datetime.datetime.strptime(ts.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return None
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for l in self.lines:
             f = [x.strip() for x in l.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
+                rows.append((self._stamp(f[0]), float(f[2]), float(f[3]), f[6:10]))
             except ValueError:
                 continue
-            for name, val in zip(names, f[5:9]):
-                if val.lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        sel = rows
+        if self.window is not None:
+            t0, t1 = self.window
+            inside = [r for r in rows if r[0] is not None and t0 - 0.05 <= r[0] <= t1 + 0.05]
+            if inside:
+                sel = inside
+        reasons = {n for r in sel for n, v in zip(names, r[3]) if v.lower() == "active"}
+        sm = [r[1] for r in sel]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": sel[-1][2] if sel else None,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "window": "timed region" if sel is not rows else "whole run"}
 
 
 def synthetic_batch(model_graph, rank: int, b: int, seed: int = 42):
@@ -170,17 +197,20 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
+    clk = ClockSampler(local_rank).start()
     for _ in range(args.warmup):
         tr.run()
     barrier()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            tr.run()
-        e1.record(stream)
-        torch.cuda.synchronize()
+    w0 = time.time()
+    e0.record(stream)
+    for _ in range(args.steps):
+        tr.run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk.mark(w0, time.time())
+    clk.stop()
     barrier()
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], device=dev)

@@ -78,13 +78,34 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-// Waiters suspend in try_wait (woken by the phase flip, or after the hint)
-// instead of spinning, so idle roles do not steal issue slots from the TMA
-// producer / MMA issuer sharing their SM sub-partition.
+// Optional suspend-time hint for try_wait (ns). Off by default: with a 10 ms hint
+// some waits slept the whole hint (a missed wake-up) and a GEMM variant crawled
+// at >1 s per launch (tools/gemm_loop.py); the hint-free loop measured the same
+// speed everywhere else.
 #ifndef WAP_MBAR_HINT
-#define WAP_MBAR_HINT 0x989680
+#define WAP_MBAR_HINT 0
 #endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#ifdef WAP_MBAR_WATCHDOG
+  // diagnostic build: report (and trap) a wait that exceeds ~1 s
+  {
+    const long long t0 = clock64();
+    while (true) {
+      uint32_t ok;
+      asm volatile(
+          "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(ok)
+          : "r"(bar), "r"(parity)
+          : "memory");
+      if (ok) return;
+      if (clock64() - t0 > 2000000000LL) {
+        printf("[watchdog] block %d thread %d stuck on mbarrier smem+0x%x parity %u\n", blockIdx.x, threadIdx.x,
+               bar, parity);
+        asm volatile("trap;");
+      }
+    }
+  }
+#endif
 #if WAP_MBAR_HINT > 0
   asm volatile(
       "{\n"

@@ -100,12 +100,24 @@ struct Cfg {
   static constexpr int TMEM_A_SLOTS = PREC == 3 ? (512 - A_COL0) / 64 : 64;
   static constexpr int STAGES_SMEM = kSmemBudget / STAGE_BYTES;
   // smem stages (TMA prefetch depth) and TMEM A slots (split -> MMA) are separate rings
-  static constexpr int A_SLOTS = PREC == 3 ? (TMEM_A_SLOTS > 8 ? 8 : TMEM_A_SLOTS) : 1;
-  static constexpr int STAGES = WIN ? 6 : (STAGES_SMEM > 8 ? 8 : STAGES_SMEM);
+#ifndef WAP_MAX_A_SLOTS
+#define WAP_MAX_A_SLOTS 8
+#endif
+  // Splitter groups take alternate k-steps and wait on stage / A-slot mbarriers by
+  // parity. A group must observe every phase of each barrier it waits on: with an
+  // odd ring size it would use a barrier only every other phase and a parity wait
+  // could pass on the phase before the one it needs (ABA). So both rings are a
+  // multiple of kSplitGroups (each group then owns a fixed subset of slots).
+  static constexpr int ring_round(int n) { return PREC == 3 ? n / kSplitGroups * kSplitGroups : n; }
+  static constexpr int A_SLOTS =
+      PREC == 3 ? ring_round(TMEM_A_SLOTS > WAP_MAX_A_SLOTS ? WAP_MAX_A_SLOTS : TMEM_A_SLOTS) : 1;
+  static constexpr int STAGES = WIN ? 6 : ring_round(STAGES_SMEM > 8 ? 8 : STAGES_SMEM);
   static constexpr int TMEM_COLS = PREC == 3 ? 512 : ((2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512));
   static constexpr int THREADS = PREC == 3 ? 256 + 256 * kSplitGroups : 256;  // + splitter warp groups
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + kEpiStage + kBarBytes;
   static_assert(STAGES >= 2, "need at least two pipeline stages");
+  static_assert(PREC != 3 || (STAGES % kSplitGroups == 0 && A_SLOTS % kSplitGroups == 0 && A_SLOTS >= 1),
+                "3xTF32 rings must be multiples of the splitter group count");
   static_assert(B_ROWS % 32 == 0, "B rows per CTA must be a multiple of 32");
 };
 
@@ -967,7 +979,11 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           if (tap == 0 || kc == tc.kc_begin) {
             wslot = wc & 1;
             ++wc;
-            wwaited = false;
+            // every group observes every window phase, including windows it has no
+            // step in (a one-step window at a split-K boundary), so its parity waits
+            // never skip a phase
+            TW(2, mbar_wait(smem_u32(&wfull_bar[wslot]), ((wc - 1) >> 1) & 1));
+            wwaited = true;
           }
           last_in_win = (tap == ntaps - 1) || (kc == tc.kc_end - 1);
         }

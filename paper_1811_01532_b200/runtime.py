@@ -33,6 +33,7 @@ every constructor raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -617,6 +618,9 @@ class Program:
                     call = GemmCall(d, device=self.device)
                 except Exception:
                     continue
+                if os.environ.get("WAP_AUTOTUNE_LOG"):
+                    print(f"autotune {st.name} M={d.M} N={d.N} K={d.K} cluster={cluster} window={window} bn={bn}",
+                          flush=True)
                 N.check(self.L.wap_gemm_plan_run(call._plan, s), "autotune warm-up")
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
