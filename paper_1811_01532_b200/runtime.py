@@ -1127,6 +1127,49 @@ class Program:
                 src = st
             N.check(self.L.wap_pack(src.data_ptr(), t.layout(), t.ptr, 0, s), "pack")
 
+    def bind_overlapped(self, values: dict, copy_stream) -> None:
+        """Training-loop input path with the host->device copy off the critical path.
+
+        The H2D copy of this step's shard runs on `copy_stream` into a dense staging
+        buffer, so it overlaps the previous step still running on the compute
+        stream; the compute stream then waits for it and packs / copies staging
+        into the input buffers the step's kernels (or captured graph) read. The
+        next call's H2D waits only until this pack has consumed the staging."""
+        torch = self.torch
+        if not hasattr(self, "_ov_staging"):
+            self._ov_staging = {}
+            self._ov_free = None
+        compute = torch.cuda.current_stream(self.device)
+        if self._ov_free is not None:
+            copy_stream.wait_event(self._ov_free)
+        staged = {}
+        with torch.cuda.stream(copy_stream):
+            for k, v in values.items():
+                t = self.t[k]
+                n = int(np.prod(t.dims))
+                if isinstance(v, np.ndarray):
+                    v = torch.from_numpy(v)
+                if v.dtype != torch.float32:
+                    raise EvalError(f"binding {k!r} must be float32 for the async path")
+                st = self._ov_staging.get(k)
+                if st is None:
+                    st = self._ov_staging[k] = torch.empty(n, dtype=torch.float32, device=self.device)
+                st.copy_(v.reshape(-1), non_blocking=True)
+                staged[k] = st
+        ev = torch.cuda.Event()
+        ev.record(copy_stream)
+        compute.wait_event(ev)
+        s = N.stream_ptr(compute)
+        for k, st in staged.items():
+            t = self.t[k]
+            n = st.numel()
+            if t.pad == 0 and t.ld == t.dims[-1]:
+                t.buf[:n].copy_(st, non_blocking=True)
+            else:
+                N.check(self.L.wap_pack(st.data_ptr(), t.layout(), t.ptr, 0, s), "pack")
+        self._ov_free = torch.cuda.Event()
+        self._ov_free.record(compute)
+
     def fetch(self, nid: str) -> np.ndarray:
         torch = self.torch
         t = self.t[nid]

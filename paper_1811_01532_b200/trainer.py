@@ -153,5 +153,24 @@ class Trainer:
         loss = self.prog.t[self.loss_id].buf[:1]
         return float(loss.item()) if fetch else loss
 
+    def step_async(self, batch: dict) -> None:
+        """One step from pinned host buffers without host synchronisation: the H2D
+        copy of `batch` runs on a copy stream (overlapping the previous step), the
+        step runs on the compute stream, and the loss is copied to a pinned host
+        scalar (D2H) behind it. `last_loss()` waits for and returns that value."""
+        torch = self.torch
+        if not hasattr(self, "copy_stream"):
+            self.copy_stream = torch.cuda.Stream()
+            self._loss_host = torch.empty(1, dtype=torch.float32, pin_memory=True)
+            self._loss_ev = torch.cuda.Event()
+        self.prog.bind_overlapped(batch, self.copy_stream)
+        self.run()
+        self._loss_host.copy_(self.prog.t[self.loss_id].buf[:1], non_blocking=True)
+        self._loss_ev.record()
+
+    def last_loss(self) -> float:
+        self._loss_ev.synchronize()
+        return float(self._loss_host[0])
+
     def variables(self) -> dict[str, np.ndarray]:
         return {n.id: self.prog.fetch(n.id) for n in self.view if n.kind is OpKind.VARIABLE}

@@ -48,3 +48,24 @@ def test_trainer_graph_step_matches_execute(cuda, net, kw):
     for vid, val in got.items():
         dev = O.relative_deviation(val, ref[f"{vid}_upd"])
         assert dev < 1e-6, (vid, dev)
+
+
+def test_step_async_matches_step(cuda):
+    """The overlapped input path (H2D on a copy stream, async loss D2H) computes the
+    same two consecutive steps as the synchronous Trainer.step."""
+    g = models.MODELS["alexnet"](batch=4, image=99)
+    b1, b2 = _bindings(g, seed=11), _bindings(g, seed=12)
+    variables = {k: v for k, v in b1.items() if k not in ("images", "labels")}
+    tp = trainer.plan_training(g, 1, planner.load_profile("b200"), force_d=1)
+    pinned = [{k: torch.from_numpy(b[k]).pin_memory() for k in ("images", "labels")} for b in (b1, b2)]
+    ta = trainer.Trainer(tp, variables=variables, use_graph=True)
+    ta.step_async(pinned[0])
+    ta.step_async(pinned[1])
+    la = ta.last_loss()
+    tb = trainer.Trainer(tp, variables=variables, use_graph=True)
+    tb.step(pinned[0])
+    lb = tb.step(pinned[1], fetch=True)
+    assert la == lb
+    va, vb = ta.variables(), tb.variables()
+    for k in va:
+        assert np.array_equal(va[k], vb[k]), k
