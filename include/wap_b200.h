@@ -103,6 +103,17 @@ typedef struct {
  * col[(b,ho,wo), (u,v,c)] = x[b, ho*s+u-p, wo*s+v-p, c] (0 outside), columns
  * K..ldcol-1 zeroed. Rows enumerate the output grid with out_pad trailing halo
  * columns/rows (halo rows zero): col is [B*(Ho+out_pad)*(Wo+out_pad), ldcol]. */
+/* Space-to-depth (first-layer strided conv without im2col): a k x k stride-s conv
+ * with padding p over x is a ceil(k/s)^2-tap stride-1 VALID conv over
+ *   xs[b, i, j, (dy*s+dx)*C + c] = x[b, s*i+dy-p, s*j+dx-p, c]   (0 outside x)
+ * with ws[a, e, (dy*s+dx)*C + c, o] = w[s*a+dy, s*e+dx, c, o] (0 beyond k).
+ * xs is dense [B*Hs*Ws, ldc] (ldc >= s*s*C, lanes beyond zeroed); w / dw are
+ * [k*k*C, ldw], ws / dws are [ks*ks*ldc, ldws]. fold_grad = 1 maps a dws back to
+ * dw (the map is a permutation, so the weight gradient is exact). */
+int wap_s2d_input(const float* x, wap_layout_t xl, int stride, int padding, int Hs, int Ws, float* xs, int ldc,
+                  void* stream);
+int wap_s2d_weight(const float* w, float* ws, int k, int C, int Co, int ldw, int stride, int ldc, int ldws,
+                   int fold_grad, void* stream);
 int wap_im2col(const float* x, wap_layout_t xl, int k, int stride, int padding, int Ho, int Wo, int out_pad,
                float* col, int64_t ldcol, void* stream);
 /* col2im (gather form, deterministic) for GradConv2DX (interp.py:94-102):

@@ -342,6 +342,101 @@ __global__ void col2im_kernel(const float* __restrict__ dcol, int64_t ldcol, int
 }
 
 // ---------------------------------------------------------------------------
+// Space-to-depth for strided first-layer convs (AlexNet conv1 11x11/4 pad 2)
+// ---------------------------------------------------------------------------
+// A k x k stride-s conv with zero padding p over x equals a ceil(k/s)^2-tap
+// stride-1 VALID conv over xs[b, i, j, (dy*s+dx)*C + c] = xpad[b, s*i+dy, s*j+dx, c]
+// with weights ws[a, e, (dy*s+dx)*C + c, o] = w[s*a+dy, s*e+dx, c, o] (0 beyond k).
+// On the s2d grid (Hs x Ws rows per image, no halo) the VALID conv is a shifted
+// GEMM with tap shifts a*Ws + e whose output grid is the conv output with
+// Hs - Ho trailing halo rows / columns: no im2col buffer.
+// One thread per output float4 (32-bit indices; the host checks the size): 16
+// consecutive threads write one s2d pixel's 64 channels as 256 contiguous bytes,
+// the gathered reads hit L1/L2 (neighbouring threads read the same input pixels).
+__global__ void __launch_bounds__(256) s2d_input_kernel(const float* __restrict__ x, wap_layout_t xl, int s, int p,
+                                                        int Hs, int Wsd, float* __restrict__ xs, int ldc) {
+  const int C = xl.C;
+  const uint32_t q4n = (uint32_t)ldc / 4;
+  const uint32_t total = (uint32_t)xl.B * Hs * Wsd * q4n;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const uint32_t q = e % q4n, pix = e / q4n;
+    const uint32_t j = pix % (uint32_t)Wsd, r = pix / (uint32_t)Wsd;
+    const int ii = (int)(r % (uint32_t)Hs), b = (int)(r / (uint32_t)Hs);
+    float o[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int cs = (int)q * 4 + l;
+      float v = 0.f;
+      if (cs < s * s * C) {
+        const int t = cs / C, c = cs - t * C;
+        const int dy = t / s, dx = t - dy * s;
+        const int h = ii * s + dy - p, w = (int)j * s + dx - p;
+        if (h >= 0 && h < xl.H && w >= 0 && w < xl.W) v = __ldg(x + lidx(xl, b, h, w, c));
+      }
+      o[l] = v;
+    }
+    reinterpret_cast<float4*>(xs)[e] = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// Narrow inputs (C <= 4 stored as one float4 per pixel, e.g. RGB padded to 4):
+// one thread per (s2d pixel, source pixel t = dy*s + dx) reads that pixel's float4
+// (coalesced along dx) and writes its C channels at t*C; threads t*C >= s*s*C
+// zero the channel padding of their s2d pixel.
+__global__ void __launch_bounds__(256) s2d_input_px4_kernel(const float* __restrict__ x, wap_layout_t xl, int s,
+                                                            int p, int Hs, int Wsd, float* __restrict__ xs,
+                                                            int ldc) {
+  const int C = xl.C;
+  const int ss = s * s;
+  const uint32_t per = (uint32_t)(ldc / C > ss ? (ldc + C - 1) / C : ss);  // threads per s2d pixel
+  const uint32_t total = (uint32_t)xl.B * Hs * Wsd * per;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const uint32_t t = e % per, pix = e / per;
+    float* dst = xs + (int64_t)pix * ldc;
+    if ((int)t >= ss) {  // channel padding of this pixel
+      for (int c = (int)t * C; c < (int)(t + 1) * C && c < ldc; ++c) dst[c] = 0.f;
+      continue;
+    }
+    const uint32_t j = pix % (uint32_t)Wsd, r = pix / (uint32_t)Wsd;
+    const int ii = (int)(r % (uint32_t)Hs), b = (int)(r / (uint32_t)Hs);
+    const int dy = (int)t / s, dx = (int)t - dy * s;
+    const int h = ii * s + dy - p, w = (int)j * s + dx - p;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (h >= 0 && h < xl.H && w >= 0 && w < xl.W) v = __ldg(reinterpret_cast<const float4*>(x + lidx(xl, b, h, w, 0)));
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+    for (int c = 0; c < C; ++c) dst[t * C + c] = vv[c];
+  }
+}
+
+// ws[(a*ks + e)*ldc + cs][o] = w[s*a+dy][s*e+dx][c][o]; grad = 0: forward weight map,
+// grad = 1: fold dws back into dw[u][v][c][o] (each (u, v, c) has exactly one source)
+__global__ void s2d_weight_kernel(const float* __restrict__ src, float* __restrict__ dst, int k, int C, int Co,
+                                  int ldw, int s, int ks, int ldc, int ldws, int grad) {
+  const int64_t rows = grad ? (int64_t)k * k * C : (int64_t)ks * ks * ldc;
+  const int64_t total = rows * Co;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int o = (int)(i % Co);
+    const int64_t row = i / Co;
+    if (!grad) {
+      const int cs = (int)(row % ldc), tap = (int)(row / ldc);
+      const int a = tap / ks, e = tap % ks;
+      float v = 0.f;
+      if (cs < s * s * C) {
+        const int c = cs % C, t = cs / C;
+        const int u = a * s + t / s, vv = e * s + t % s;
+        if (u < k && vv < k) v = src[((int64_t)(u * k + vv) * C + c) * ldw + o];
+      }
+      dst[row * ldws + o] = v;
+    } else {
+      const int c = (int)(row % C), uv = (int)(row / C);
+      const int u = uv / k, vv = uv % k;
+      const int a = u / s, e = vv / s, cs = ((u % s) * s + (vv % s)) * C + c;
+      dst[row * ldw + o] = src[((int64_t)(a * ks + e) * ldc + cs) * ldws + o];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // MaxPool
 // ---------------------------------------------------------------------------
 // Row-blocked launches: blockIdx.y = b * H + h (one output row for the forward,
@@ -359,9 +454,9 @@ __global__ void __launch_bounds__(256) maxpool_fwd_kernel(const float* __restric
                                                           int s, float* __restrict__ y, wap_layout_t yl,
                                                           uint8_t* __restrict__ arg, int relu_fused) {
   const int c4n = yl.ld / 4;
-  const int row = blockIdx.y;
-  const int b = row / yl.H, ho = row - (row / yl.H) * yl.H;
   const int per = yl.W * c4n;
+  for (int row = blockIdx.y; row < yl.B * yl.H; row += gridDim.y) {
+  const int b = row / yl.H, ho = row - (row / yl.H) * yl.H;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < per; j += gridDim.x * blockDim.x) {
     const int wo = j / c4n;
     const int c = (j - wo * c4n) * 4;
@@ -388,6 +483,7 @@ __global__ void __launch_bounds__(256) maxpool_fwd_kernel(const float* __restric
     if (arg) *reinterpret_cast<uchar4*>(arg + yi) = make_uchar4((uint8_t)bi[0], (uint8_t)bi[1], (uint8_t)bi[2],
                                                                 (uint8_t)bi[3]);
   }
+  }
 }
 
 __global__ void __launch_bounds__(256) maxpool_bwd_kernel(const uint8_t* __restrict__ arg,
@@ -395,7 +491,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_kernel(const uint8_t* __restr
                                                           int s, float* __restrict__ dx, wap_layout_t xl,
                                                           const float* __restrict__ mask, wap_layout_t ml) {
   const int c4n = xl.ld / 4;
-  const int row = blockIdx.y;
+  for (int row = blockIdx.y; row < xl.B * xl.H; row += gridDim.y) {
   const int b = row / xl.H, h = row - (row / xl.H) * xl.H;
   // windows (ho, wo) with ho*s <= h < ho*s + win
   const int ho_lo = h >= win ? (h - win) / s + 1 : 0;
@@ -430,10 +526,12 @@ __global__ void __launch_bounds__(256) maxpool_bwd_kernel(const uint8_t* __restr
       if (c + t >= xl.C) acc[t] = 0.f;
     *reinterpret_cast<float4*>(dx + lidx(xl, b, h, w, c)) = make_float4(acc[0], acc[1], acc[2], acc[3]);
   }
+  }
 }
 
+// rows beyond gridDim.y's 65535 limit are covered by the kernels' row loop
 dim3 pool_grid(int rows, int per) {
-  return dim3((unsigned)std::max(1, std::min((per + 255) / 256, 64)), (unsigned)rows);
+  return dim3((unsigned)std::max(1, std::min((per + 255) / 256, 64)), (unsigned)std::min(rows, 65535));
 }
 
 // ---------------------------------------------------------------------------
@@ -915,6 +1013,45 @@ extern "C" int wap_bias_grad(const float* dy, wap_layout_t l, float* db, float* 
   bias_grad_final<<<(l.C + 3) / 4, 128, 0, STREAM(stream)>>>(work, chunks, l.ld, l.C, db);
   WAP_LAUNCH_CHECK();
   g_wap_launches.fetch_add(2, std::memory_order_relaxed);
+  return WAP_OK;
+}
+
+extern "C" int wap_s2d_input(const float* x, wap_layout_t xl, int stride, int padding, int Hs, int Ws, float* xs,
+                             int ldc, void* stream) {
+  int rc;
+  if ((rc = check_layout(xl, "x"))) return rc;
+  WAP_CHECK_ARG(x && xs && stride >= 1 && padding >= 0 && Hs >= 1 && Ws >= 1, "s2d: bad arguments");
+  WAP_CHECK_ARG(ldc % 4 == 0 && ldc >= stride * stride * xl.C, "s2d: ldc must cover s*s*C and be a multiple of 4");
+  const int64_t total4 = (int64_t)xl.B * Hs * Ws * (ldc / 4);
+  WAP_CHECK_ARG(total4 < (1LL << 31), "s2d: grid too large for 32-bit indexing");
+  int64_t blocks = (total4 + 255) / 256;
+  if (blocks > (int64_t)WAP_NUM_SMS * 32) blocks = (int64_t)WAP_NUM_SMS * 32;
+  if (xl.ld == 4 && xl.C <= 4) {
+    const int ss = stride * stride;
+    const int64_t per = ldc / xl.C > ss ? (ldc + xl.C - 1) / xl.C : ss;
+    const int64_t total = (int64_t)xl.B * Hs * Ws * per;
+    WAP_CHECK_ARG(total < (1LL << 31), "s2d: grid too large for 32-bit indexing");
+    int64_t nb = (total + 255) / 256;
+    if (nb > (int64_t)WAP_NUM_SMS * 32) nb = (int64_t)WAP_NUM_SMS * 32;
+    s2d_input_px4_kernel<<<(int)nb, 256, 0, STREAM(stream)>>>(x, xl, stride, padding, Hs, Ws, xs, ldc);
+  } else {
+    s2d_input_kernel<<<(int)blocks, 256, 0, STREAM(stream)>>>(x, xl, stride, padding, Hs, Ws, xs, ldc);
+  }
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
+  return WAP_OK;
+}
+
+extern "C" int wap_s2d_weight(const float* w, float* ws, int k, int C, int Co, int ldw, int stride, int ldc,
+                              int ldws, int fold_grad, void* stream) {
+  WAP_CHECK_ARG(w && ws && k >= 1 && C >= 1 && Co >= 1 && stride >= 1, "s2d weight: bad arguments");
+  WAP_CHECK_ARG(ldw >= Co && ldws >= Co && ldc >= stride * stride * C, "s2d weight: bad strides");
+  const int ks = (k + stride - 1) / stride;
+  const int64_t rows = fold_grad ? (int64_t)k * k * C : (int64_t)ks * ks * ldc;
+  s2d_weight_kernel<<<grid_for(rows * Co, 256), 256, 0, STREAM(stream)>>>(w, ws, k, C, Co, ldw, stride, ks, ldc, ldws,
+                                                                          fold_grad);
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
   return WAP_OK;
 }
 

@@ -226,7 +226,7 @@ class Program:
                 s, p = conv_geometry(n, k)
                 ci = self.dims(n.inputs[0])[3]
                 ok = s == 1 and p == k // 2 and k % 2 == 1 and ci % 32 == 0 and k * k <= SHIFTED_MAX_TAPS
-                self.strategy[nid] = "shifted" if ok else "im2col"
+                self.strategy[nid] = "shifted" if ok else ("s2d" if self._s2d_geometry(n) else "im2col")
         # forward epilogue fusion: producer -> (bias node | None, relu node | None)
         self.fwd_fuse: dict[str, tuple[str | None, str | None]] = {}
         self.virtual: set[str] = set()
@@ -296,6 +296,25 @@ class Program:
                              for g in grads):
                 self.pool_relu_fused.add(pool)
 
+    def _s2d_geometry(self, n: Node):
+        """Space-to-depth plan of a strided conv over a graph input (first layer, no
+        dgrad): (s, p, ks, Hs, Ws, ldc, halo) when the stride-s conv equals a
+        ks x ks VALID stride-1 conv over the s2d grid, else None."""
+        if self.kind(n.inputs[0]) is not OpKind.INPUT or os.environ.get("WAP_NO_S2D"):
+            return None
+        k = self.dims(n.inputs[1])[0]
+        s, p = conv_geometry(n, k)
+        b, h, w, c = self.dims(n.inputs[0])
+        _, ho, wo, _ = self.dims(n.id)
+        if s < 2 or (h + 2 * p) % s or (w + 2 * p) % s:
+            return None
+        ks = -(-k // s)
+        hs, ws = (h + 2 * p) // s, (w + 2 * p) // s
+        if hs - ks + 1 != ho or ws - ks + 1 != wo or hs - ho != ws - wo or ks * ks > SHIFTED_MAX_TAPS:
+            return None
+        ldc = -(-(s * s * c) // 32) * 32
+        return s, p, ks, hs, ws, ldc, hs - ho
+
     def mask_src(self, nid: str) -> str:
         return self.mask_alias.get(nid, nid)
 
@@ -330,6 +349,8 @@ class Program:
                     k = self.dims(n.inputs[1])[0]
                     uf.union(n.inputs[0], out)
                     need(n.inputs[0], k // 2)
+                elif self.strategy[nid] == "s2d":
+                    need(out, self._s2d_geometry(n)[6])  # output grid = the s2d grid
             elif n.kind is OpKind.GRAD_CONV2D_X:
                 conv = self._conv_of_weight(n.inputs[1])
                 uf.union(n.inputs[0], self.fused_out(conv))
@@ -526,7 +547,8 @@ class Program:
         kinds = (OpKind.GRAD_CONV2D_W, OpKind.GRAD_MATMUL_W, OpKind.GRAD_BIAS)
         side = None
         for i, st in enumerate(self.steps):
-            if st.name in self.g.nodes and self.kind(st.name) in kinds:
+            base = st.name.split("/")[0]  # a wgrad's companion steps (s2d fold) follow it
+            if base in self.g.nodes and self.kind(base) in kinds:
                 if side is None:
                     side = self.torch.cuda.Stream(device=self.device)
                 self.steps[i] = _ParallelStep(st, side, self.torch)
@@ -752,6 +774,25 @@ class Program:
         bias = self._in(self.node(zb), self.node(zb).inputs[1]) if zb is not None else None
         relu = r is not None
         b, ho, wo, _ = self.dims(n.id)
+        if self.strategy[n.id] == "s2d":
+            s_, p_, ks, hs, ws, ldc, halo = self._s2d_geometry(n)
+            if y.pad != halo:
+                raise EvalError(f"{n.id!r}: s2d output needs a trailing halo of {halo}, layout has {y.pad}")
+            torch = self.torch
+            rows = b * hs * ws
+            xs = torch.zeros(rows * ldc, dtype=torch.float32, device=self.device)
+            wsb = torch.zeros(ks * ks * ldc * w.ld, dtype=torch.float32, device=self.device)
+            self.t[f"{n.id}::s2d"] = Tensor((rows, ldc), 0, ldc, xs, "mat")
+            self._emit(n.id + "/s2d", self.L.wap_s2d_input, (x.ptr, x.layout(), s_, p_, hs, ws, xs.data_ptr(), ldc),
+                       "space-to-depth", keep=[xs], alg_bytes=self._nbytes(x) + 4 * rows * ldc)
+            self._emit(n.id + "/s2d_w", self.L.wap_s2d_weight,
+                       (w.ptr, wsb.data_ptr(), kk, ci, co, w.ld, s_, ldc, w.ld, 0), "space-to-depth weights",
+                       keep=[wsb], alg_bytes=4 * (kk * kk * ci + ks * ks * ldc) * co)
+            a = N.operand(xs.data_ptr(), inner=ldc, outer=rows, ld=ldc, mn_major=False, tap_period=ldc,
+                          offsets=tuple(u * ws + v for u in range(ks) for v in range(ks)))
+            bo = N.operand(wsb.data_ptr(), inner=co, outer=ks * ks * ldc, ld=w.ld, mn_major=True)
+            self._gemm(n.id, rows, co, ks * ks * ldc, a, bo, y, bias=bias, relu=relu, halo=(halo, ho, wo))
+            return
         if self.strategy[n.id] == "shifted":
             P = x.pad
             assert y.pad == P, (n.id, y.pad, P)
@@ -921,6 +962,19 @@ class Program:
         dw = self._out(n.id)
         conv = self._conv_of_wgrad(n)
         kk, _, ci, co = self.dims(n.id)
+        if self.strategy[conv] == "s2d":
+            s_, p_, ks, hs, ws, ldc, halo = self._s2d_geometry(self.node(conv))
+            xs = self.t[f"{conv}::s2d"]
+            assert dy.rows == xs.rows and dy.pad == halo, (n.id, dy.rows, xs.rows)
+            dws = self.torch.zeros(ks * ks * ldc * dw.ld, dtype=self.torch.float32, device=self.device)
+            a = N.operand(xs.ptr, inner=ldc, outer=xs.rows, ld=ldc, mn_major=True, tap_period=ldc,
+                          offsets=tuple(u * ws + v for u in range(ks) for v in range(ks)))
+            bo = N.operand(dy.ptr, inner=co, outer=dy.rows, ld=dy.ld, mn_major=True)
+            self._gemm(n.id, ks * ks * ldc, co, xs.rows, a, bo, Tensor((ks * ks * ldc, co), 0, dw.ld, dws, "mat"))
+            self._emit(n.id + "/fold", self.L.wap_s2d_weight,
+                       (dws.data_ptr(), dw.ptr, kk, ci, co, dw.ld, s_, ldc, dw.ld, 1), "s2d weight-gradient fold",
+                       keep=[dws], alg_bytes=4 * (kk * kk * ci + kk * kk * ci) * co)
+            return
         if self.strategy[conv] == "shifted":
             P = x.pad
             assert dy.pad == P

@@ -52,7 +52,7 @@ def test_trainer_graph_step_matches_execute(cuda, net, kw):
 
 def test_step_async_matches_step(cuda):
     """The overlapped input path (H2D on a copy stream, async loss D2H) computes the
-    same two consecutive steps as the synchronous Trainer.step."""
+    same two consecutive steps as the synchronous Trainer.step (to fp32 rounding)."""
     g = models.MODELS["alexnet"](batch=4, image=99)
     b1, b2 = _bindings(g, seed=11), _bindings(g, seed=12)
     variables = {k: v for k, v in b1.items() if k not in ("images", "labels")}
@@ -65,7 +65,9 @@ def test_step_async_matches_step(cuda):
     tb = trainer.Trainer(tp, variables=variables, use_graph=True)
     tb.step(pinned[0])
     lb = tb.step(pinned[1], fetch=True)
-    assert la == lb
+    # the two Trainers autotune independently (split-K / cluster choices can differ,
+    # changing fp32 summation order), so agreement is to rounding, not bitwise
+    assert abs(la - lb) <= 1e-6 * max(1.0, abs(lb))
     va, vb = ta.variables(), tb.variables()
     for k in va:
-        assert np.array_equal(va[k], vb[k]), k
+        assert O.relative_deviation(va[k], vb[k]) < 1e-6, k
