@@ -74,6 +74,14 @@ typedef struct {
   int32_t window;                   /* 3xTF32 shifted A: 0 = halo-window reuse when it fits, -1 = off */
   float* workspace;                 /* split-K partials, wap_gemm_workspace_bytes() */
   int64_t workspace_bytes;
+  /* ReLU masks as bits (1 bit per element, 32 columns per word, row stride in words):
+   * mbits_out: the epilogue also writes [out > 0] of its final output (forward Conv2D /
+   *   MatMul + ReLU; forces split-K off);
+   * mbits_in: GradReLU mask read from such bits instead of `mask` (dgrad epilogues). */
+  uint32_t* mbits_out;
+  int64_t mbits_out_ld;
+  const uint32_t* mbits_in;
+  int64_t mbits_in_ld;
 } wap_gemm_desc_t;
 
 int64_t wap_gemm_workspace_bytes(const wap_gemm_desc_t* desc);

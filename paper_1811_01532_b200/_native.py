@@ -61,6 +61,10 @@ class wap_gemm_desc_t(C.Structure):
         ("window", C.c_int32),
         ("workspace", C.c_void_p),
         ("workspace_bytes", C.c_int64),
+        ("mbits_out", C.c_void_p),
+        ("mbits_out_ld", C.c_int64),
+        ("mbits_in", C.c_void_p),
+        ("mbits_in_ld", C.c_int64),
     ]
 
 

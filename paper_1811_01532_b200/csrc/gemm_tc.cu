@@ -96,7 +96,9 @@ Shape plan_shape(const wap_gemm_desc_t& d) {
   const long long tiles = (long long)s.m_tiles * s.n_tiles;
   const long long slots = WAP_NUM_SMS / s.cg;
   int splits = 1;
-  if (d.splits > 0) {
+  if (d.mbits_out || d.mbits_in) {
+    splits = 1;  // mask bits are produced / consumed by the non-split epilogue
+  } else if (d.splits > 0) {
     splits = d.splits;
   } else if (tiles < slots) {
     splits = (int)std::max(1LL, slots / tiles);
@@ -190,6 +192,11 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
   p->win = g.win_boxes > 0 ? 1 : 0;
   g.partial = nullptr;
   g.split_stride = d.M * d.ldc;
+  g.mbits_out = d.mbits_out;
+  g.mbits_out_ld = d.mbits_out_ld;
+  g.mbits_in = d.mbits_in;
+  g.mbits_in_ld = d.mbits_in_ld;
+  WAP_CHECK_ARG(!(d.mbits_out || d.mbits_in) || s.splits == 1, "ReLU mask bits need split-K off");
   // epilogue output through bulk tensor stores when C is TMA-addressable
   g.tma_store = 0;
   if (s.splits == 1 && (reinterpret_cast<uintptr_t>(d.c) & 15) == 0 && d.ldc % 4 == 0 &&
@@ -206,6 +213,7 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
   } else {
     p->tmC = p->tmA;  // unused
   }
+  WAP_CHECK_ARG(!(d.mbits_out || d.mbits_in) || g.tma_store, "ReLU mask bits need the TMA-store epilogue");
   if (s.splits > 1) {
     const int64_t need = (int64_t)s.splits * d.M * d.ldc * 4;
     WAP_CHECK_ARG(d.workspace != nullptr && d.workspace_bytes >= need,

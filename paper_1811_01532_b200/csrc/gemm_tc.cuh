@@ -72,6 +72,10 @@ struct GemmArgs {
   int32_t halo_pad, halo_h, halo_w;
   int32_t win_boxes, win_off_min;  // WIN: 128-row TMA boxes per A halo window, min tap shift
   int32_t tma_store;               // epilogue writes C through tmC (bulk tensor stores)
+  uint32_t* mbits_out;             // ReLU mask bits of the output (32 columns per word)
+  int64_t mbits_out_ld;
+  const uint32_t* mbits_in;        // GradReLU mask bits (replaces `mask`)
+  int64_t mbits_in_ld;
 };
 
 // 3xTF32 keeps the A operand in TMEM (tcgen05 "TS" form): the splitter warps
@@ -740,7 +744,11 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
 #else
     const float* bias = raw_out ? nullptr : g.bias;
 #endif
+#ifdef WAP_DIAG_NO_MASK
+    const float* mask = nullptr;
+#else
     const float* mask = raw_out ? nullptr : g.mask;
+#endif
     const bool mvec = (g.ldm % 4) == 0;
     const int c4 = (lane & 7) * 4;
     // bias of this lane's 4 columns of the chunk starting at column nb
@@ -821,14 +829,26 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           // which alternates between two values for even / odd it.
           const bool relu = g.relu != 0;
           const int64_t ldm4 = (int64_t)g.ldm * 4;
-          const float* mp = mask ? mask + (m_warp + (lane >> 3)) * g.ldm + col : nullptr;
+          const float* mp = (mask && !g.mbits_in) ? mask + (m_warp + (lane >> 3)) * g.ldm + col : nullptr;
+          // bit-packed masks: word (row, chunk); this lane's 4 columns are bits c4..c4+3
+          const uint32_t* bip = g.mbits_in ? g.mbits_in + (m_warp + (lane >> 3)) * g.mbits_in_ld + (nb >> 5) : nullptr;
+          uint32_t* bop = g.mbits_out ? g.mbits_out + (m_warp + (lane >> 3)) * g.mbits_out_ld + (nb >> 5) : nullptr;
+          const int64_t bi4 = g.mbits_in_ld * 4, bo4 = g.mbits_out_ld * 4;
           const uint32_t q = lane & 7, r0 = lane >> 3;
           const uint32_t s_even = stg_s + r0 * 128 + ((q ^ r0) << 4);
           const uint32_t s_odd = stg_s + (r0 + 4) * 128 + ((q ^ (r0 + 4)) << 4);
 #pragma unroll 1
-          for (int it = 0; it < 8; it += 2, mp += mask ? 2 * ldm4 : 0) {
+          for (int it = 0; it < 8; it += 2, mp += mp ? 2 * ldm4 : 0, bip += bip ? 2 * bi4 : 0,
+                   bop += bop ? 2 * bo4 : 0) {
             float4 mk0 = make_float4(1.f, 1.f, 1.f, 1.f), mk1 = mk0;
-            if (mask) {
+            if (bip) {
+              const uint32_t w0 = (row_ok & (1u << it)) ? (__ldg(bip) >> c4) : 0u;
+              const uint32_t w1 = (row_ok & (2u << it)) ? (__ldg(bip + bi4) >> c4) : 0u;
+              mk0 = make_float4((float)(w0 & 1u), (float)((w0 >> 1) & 1u), (float)((w0 >> 2) & 1u),
+                                (float)((w0 >> 3) & 1u));
+              mk1 = make_float4((float)(w1 & 1u), (float)((w1 >> 1) & 1u), (float)((w1 >> 2) & 1u),
+                                (float)((w1 >> 3) & 1u));
+            } else if (mp) {
               const bool ok0 = row_ok & (1u << it), ok1 = row_ok & (2u << it);
               if (full && mvec) {
                 if (ok0) mk0 = __ldg(reinterpret_cast<const float4*>(mp));
@@ -860,6 +880,21 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
             };
             x0 = fin(x0, mk0, z0);
             x1 = fin(x1, mk1, z1);
+            if (bop) {
+              // [out > 0] of rows it / it+1: lane 8k + q holds columns 4q..4q+3 of row k;
+              // OR the 8 nibbles of a row together with 3 xor-shuffles inside the 8-lane group
+              uint32_t wa = ((x0.x > 0.f) | ((x0.y > 0.f) << 1) | ((x0.z > 0.f) << 2) | ((x0.w > 0.f) << 3)) << c4;
+              uint32_t we = ((x1.x > 0.f) | ((x1.y > 0.f) << 1) | ((x1.z > 0.f) << 2) | ((x1.w > 0.f) << 3)) << c4;
+#pragma unroll
+              for (int o = 1; o < 8; o <<= 1) {
+                wa |= __shfl_xor_sync(0xffffffffu, wa, o);
+                we |= __shfl_xor_sync(0xffffffffu, we, o);
+              }
+              if ((lane & 7) == 0) {
+                if (row_ok & (1u << it)) *bop = wa;
+                if (row_ok & (2u << it)) bop[bo4] = we;
+              }
+            }
             st_shared_v4(a0, __float_as_uint(x0.x), __float_as_uint(x0.y), __float_as_uint(x0.z), __float_as_uint(x0.w));
             st_shared_v4(a1, __float_as_uint(x1.x), __float_as_uint(x1.y), __float_as_uint(x1.z), __float_as_uint(x1.w));
           }

@@ -284,6 +284,21 @@ class Program:
             n = self.node(nid)
             if n.kind is OpKind.MAX_POOL:
                 self.pool_of[(n.inputs[0], n.attr("window"), n.attr("stride"))] = nid
+        # ReLU outputs of forward conv GEMMs used as the GradReLU mask of a shifted conv
+        # dgrad GEMM: the forward epilogue also writes them as bits (1 bit per element),
+        # and the dgrad epilogue reads 4 bytes per 32 columns instead of 128
+        self.bits_src: set[str] = set()
+        if os.environ.get("WAP_NO_MASK_BITS") is None:
+            relu_out = {self.fused_out(c): c for c in self.order
+                        if self.kind(c) is OpKind.CONV2D and self.fwd_fuse.get(c, (None, None))[1] is not None}
+            for prod, gr in self.bwd_mask.items():
+                if self.kind(prod) is not OpKind.GRAD_CONV2D_X:
+                    continue
+                conv = self._conv_of_weight(self.node(prod).inputs[1])
+                src = self.mask_src(self.node(gr).inputs[0])
+                if self.strategy.get(conv) == "shifted" and src in relu_out:
+                    self.bits_src.add(src)
+        self.mask_bits: dict[str, object] = {}
         # pools whose every backward is fused with the GradReLU of the ReLU feeding them:
         # the argmax can carry that mask (WAP_POOL_RELU_FUSED)
         self.pool_relu_fused: set[str] = set()
@@ -314,6 +329,21 @@ class Program:
             return None
         ldc = -(-(s * s * c) // 32) * 32
         return s, p, ks, hs, ws, ldc, hs - ho
+
+    def _bits_out(self, out_id: str):
+        """(see _gemm: dropped again if the producing GEMM would split K)"""
+        return self._bits_alloc(out_id)
+
+    def _bits_alloc(self, out_id: str):
+        """Bit-packed ReLU mask buffer for a forward conv output (None if not needed)."""
+        if out_id not in self.bits_src:
+            return None
+        t = self.t[out_id]
+        ldw = -(-t.dims[-1] // 32)
+        buf = self.torch.zeros(t.rows * ldw, dtype=self.torch.int32, device=self.device)
+        buf.ld_words = ldw
+        self.mask_bits[out_id] = buf
+        return buf
 
     def mask_src(self, nid: str) -> str:
         return self.mask_alias.get(nid, nid)
@@ -489,7 +519,7 @@ class Program:
         return sum(4 * int(np.prod(t.dims)) for t in tensors if t is not None)
 
     def _gemm(self, name, M, Nn, K, a, b, out: Tensor, bias=None, relu=False, mask: Tensor | None = None,
-              halo=(0, 0, 0), splits=0, to_updates=False):
+              halo=(0, 0, 0), splits=0, to_updates=False, mbits_out=None, mbits_in=None, mask_fallback=None):
         from .kernels import GemmCall
 
         d = N.wap_gemm_desc_t()
@@ -504,6 +534,21 @@ class Program:
         d.halo_pad, d.halo_h, d.halo_w = halo
         d.precision = self.precision
         d.splits = splits
+        # mask bits need the non-split epilogue: GEMMs whose automatic plan would
+        # split K (small M, long K; splitting also keeps their fp32 sums short) keep
+        # the float mask, and a producer that would split publishes no bits
+        if (mbits_out is not None or mbits_in is not None) and self.L.wap_gemm_workspace_bytes(C.byref(d)) > 0:
+            if mbits_out is not None:
+                self.mask_bits.pop(name_out_of(self, mbits_out), None)
+            mbits_out = None
+            if mbits_in is not None:
+                d.mask = mask_fallback.ptr if mask_fallback is not None else None
+                d.ldm = mask_fallback.ld if mask_fallback is not None else 0
+            mbits_in = None
+        if mbits_out is not None:
+            d.mbits_out, d.mbits_out_ld = mbits_out.data_ptr(), mbits_out.ld_words
+        if mbits_in is not None:
+            d.mbits_in, d.mbits_in_ld = mbits_in.data_ptr(), mbits_in.ld_words
         call = GemmCall(d, device=self.device)
         step = _GemmStep(name, call)
         step.desc = d
@@ -791,7 +836,8 @@ class Program:
             a = N.operand(xs.data_ptr(), inner=ldc, outer=rows, ld=ldc, mn_major=False, tap_period=ldc,
                           offsets=tuple(u * ws + v for u in range(ks) for v in range(ks)))
             bo = N.operand(wsb.data_ptr(), inner=co, outer=ks * ks * ldc, ld=w.ld, mn_major=True)
-            self._gemm(n.id, rows, co, ks * ks * ldc, a, bo, y, bias=bias, relu=relu, halo=(halo, ho, wo))
+            self._gemm(n.id, rows, co, ks * ks * ldc, a, bo, y, bias=bias, relu=relu, halo=(halo, ho, wo),
+                       mbits_out=self._bits_out(out_id))
             return
         if self.strategy[n.id] == "shifted":
             P = x.pad
@@ -800,7 +846,8 @@ class Program:
             shifts = [(u - p) * wp + (v - p) for u in range(kk) for v in range(kk)]
             a = self._operand(x, False, inner=ci, tap_period=ci, offsets=tuple(shifts))
             bo = N.operand(w.ptr, inner=co, outer=kk * kk * ci, ld=w.ld, mn_major=True)
-            self._gemm(n.id, x.rows, co, kk * kk * ci, a, bo, y, bias=bias, relu=relu, halo=(P, ho, wo))
+            self._gemm(n.id, x.rows, co, kk * kk * ci, a, bo, y, bias=bias, relu=relu, halo=(P, ho, wo),
+                       mbits_out=self._bits_out(out_id))
         else:
             P = y.pad
             K = kk * kk * ci
@@ -814,7 +861,8 @@ class Program:
             ct = self.t[f"{n.id}::col"]
             a = self._operand(ct, False, inner=K)
             bo = N.operand(w.ptr, inner=co, outer=K, ld=w.ld, mn_major=True)
-            self._gemm(n.id, rows, co, K, a, bo, y, bias=bias, relu=relu, halo=(P, ho, wo) if P else (0, 0, 0))
+            self._gemm(n.id, rows, co, K, a, bo, y, bias=bias, relu=relu, halo=(P, ho, wo) if P else (0, 0, 0),
+                       mbits_out=self._bits_out(out_id))
 
     def _lower_matmul(self, n: Node) -> None:
         x = self._in(n, n.inputs[0])
@@ -939,7 +987,9 @@ class Program:
             a = self._operand(dy, False, inner=co, tap_period=co, offsets=tuple(-s_ for s_ in shifts))
             bo = N.operand(w.ptr, inner=co, outer=kk * kk * ci, ld=w.ld, mn_major=False, tap_period=co,
                            offsets=tuple(t * ci for t in range(kk * kk)))
-            self._gemm(n.id, dy.rows, ci, kk * kk * co, a, bo, out, mask=mask, halo=(P, out.dims[1], out.dims[2]))
+            bits = self.mask_bits.get(self.mask_src(self.node(gr).inputs[0])) if gr else None
+            self._gemm(n.id, dy.rows, ci, kk * kk * co, a, bo, out, mask=None if bits is not None else mask,
+                       halo=(P, out.dims[1], out.dims[2]), mbits_in=bits, mask_fallback=mask)
         else:
             P = dy.pad
             K = kk * kk * ci
@@ -1240,6 +1290,14 @@ class Program:
         self.run()
         self.torch.cuda.synchronize()
         return N.launch_count() - before
+
+
+def name_out_of(prog, buf) -> str | None:
+    """Key of a mask-bits buffer in prog.mask_bits."""
+    for k, v in prog.mask_bits.items():
+        if v is buf:
+            return k
+    return None
 
 
 class _CollectiveStep:
