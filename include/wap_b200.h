@@ -111,6 +111,15 @@ typedef struct {
  * col[(b,ho,wo), (u,v,c)] = x[b, ho*s+u-p, wo*s+v-p, c] (0 outside), columns
  * K..ldcol-1 zeroed. Rows enumerate the output grid with out_pad trailing halo
  * columns/rows (halo rows zero): col is [B*(Ho+out_pad)*(Wo+out_pad), ldcol]. */
+/* Direct stride-1 first-layer conv on CUDA cores (exact fp32 FMA): x has C <= 4
+ * channels stored as one float4 per pixel; y = conv(x, w) (+bias) (ReLU) at the
+ * valid output pixels of layout yl (halo untouched). w is [k*k*C, ldw] (KKIO),
+ * Co = yl.C a multiple of 32. mbits (optional) receives the ReLU mask bits in
+ * the GEMM epilogue's format. Replaces im2col + a K = k*k*C GEMM for 3-channel
+ * inputs (VGG-16 conv1_1). */
+int wap_conv_direct(const float* x, wap_layout_t xl, const float* w, int k, int padding, int ldw,
+                    const float* bias, int relu, float* y, wap_layout_t yl, uint32_t* mbits, int64_t mbits_ld,
+                    void* stream);
 /* Space-to-depth (first-layer strided conv without im2col): a k x k stride-s conv
  * with padding p over x is a ceil(k/s)^2-tap stride-1 VALID conv over
  *   xs[b, i, j, (dy*s+dx)*C + c] = x[b, s*i+dy-p, s*j+dx-p, c]   (0 outside x)

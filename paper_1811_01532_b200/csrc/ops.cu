@@ -437,6 +437,81 @@ __global__ void s2d_weight_kernel(const float* __restrict__ src, float* __restri
 }
 
 // ---------------------------------------------------------------------------
+// Direct first-layer conv (Ci <= 4, one float4 per input pixel): CUDA-core fp32
+// ---------------------------------------------------------------------------
+// A 3-channel stride-1 conv has K = k*k*3 = 27: as a GEMM it is one k-step per
+// 128-row tile behind an im2col pass, so its cost is all epilogue and im2col
+// traffic. Here each thread computes one output pixel x 32 output channels with
+// exact fp32 FMAs (weights of its 32 channels broadcast from shared memory),
+// applies bias / ReLU and writes the pixel's 32 channels; halo rows are untouched.
+template <int KT, int CT>  // compile-time filter size / channels (0: runtime k, xl.C)
+__global__ void __launch_bounds__(256) conv_direct_kernel(const float* __restrict__ x, wap_layout_t xl,
+                                                          const float* __restrict__ w, int k_rt, int p, int ldw,
+                                                          const float* __restrict__ bias, int relu,
+                                                          float* __restrict__ y, wap_layout_t yl,
+                                                          uint32_t* __restrict__ mbits, int64_t mbits_ld) {
+  extern __shared__ __align__(16) float ws[];  // [k*k*Ci][32] weights of this channel group, then 32 biases
+  const int C = CT ? CT : xl.C;
+  const int k = KT ? KT : k_rt;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = blockIdx.y;  // 32-channel output group
+  const int K = k * k * C;
+  for (int i = threadIdx.x; i < K * 32; i += blockDim.x) ws[i] = w[(int64_t)(i >> 5) * ldw + grp * 32 + (i & 31)];
+  if (threadIdx.x < 32) ws[K * 32 + threadIdx.x] = bias ? bias[grp * 32 + threadIdx.x] : 0.f;
+  __syncthreads();
+  const float4* ws4 = reinterpret_cast<const float4*>(ws);
+  const uint32_t npix = (uint32_t)yl.B * yl.H * yl.W;
+  for (uint32_t pix = (blockIdx.x * 8 + warp) * 32 + lane; pix < npix; pix += gridDim.x * 256) {
+    const uint32_t wq = pix % (uint32_t)yl.W, r = pix / (uint32_t)yl.W;
+    const int h = (int)(r % (uint32_t)yl.H), bb = (int)(r / (uint32_t)yl.H), wo = (int)wq;
+    float acc[32];
+#pragma unroll
+    for (int o4 = 0; o4 < 8; ++o4) {
+      const float4 bq = ws4[K * 8 + o4];
+      acc[4 * o4] = bq.x; acc[4 * o4 + 1] = bq.y; acc[4 * o4 + 2] = bq.z; acc[4 * o4 + 3] = bq.w;
+    }
+#pragma unroll
+    for (int u = 0; u < (KT ? KT : 16); ++u) {
+      if (!KT && u >= k) break;
+      const int hi = h + u - p;
+#pragma unroll
+      for (int v = 0; v < (KT ? KT : 16); ++v) {
+        if (!KT && v >= k) break;
+        const int wi = wo + v - p;
+        float4 xv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (hi >= 0 && hi < xl.H && wi >= 0 && wi < xl.W)
+          xv = __ldg(reinterpret_cast<const float4*>(x + lidx(xl, bb, hi, wi, 0)));
+        const float xa[4] = {xv.x, xv.y, xv.z, xv.w};
+        const float4* wt = ws4 + (u * k + v) * C * 8;
+#pragma unroll
+        for (int c = 0; c < (CT ? CT : 4); ++c) {
+          if (!CT && c >= C) break;
+#pragma unroll
+          for (int o4 = 0; o4 < 8; ++o4) {
+            const float4 wq4 = wt[c * 8 + o4];  // broadcast: every lane reads the same 16 bytes
+            acc[4 * o4] = fmaf(xa[c], wq4.x, acc[4 * o4]);
+            acc[4 * o4 + 1] = fmaf(xa[c], wq4.y, acc[4 * o4 + 1]);
+            acc[4 * o4 + 2] = fmaf(xa[c], wq4.z, acc[4 * o4 + 2]);
+            acc[4 * o4 + 3] = fmaf(xa[c], wq4.w, acc[4 * o4 + 3]);
+          }
+        }
+      }
+    }
+    const int64_t yrow = ((int64_t)bb * (yl.H + yl.pad) + h) * (yl.W + yl.pad) + wo;
+    float* dst = y + yrow * yl.ld + grp * 32;
+    uint32_t bits = 0;
+#pragma unroll
+    for (int o = 0; o < 32; o += 4) {
+      float4 q = make_float4(acc[o], acc[o + 1], acc[o + 2], acc[o + 3]);
+      if (relu) q = make_float4(fmaxf(q.x, 0.f), fmaxf(q.y, 0.f), fmaxf(q.z, 0.f), fmaxf(q.w, 0.f));
+      bits |= ((q.x > 0.f) << o) | ((q.y > 0.f) << (o + 1)) | ((q.z > 0.f) << (o + 2)) | ((q.w > 0.f) << (o + 3));
+      *reinterpret_cast<float4*>(dst + o) = q;
+    }
+    if (mbits) mbits[yrow * mbits_ld + grp] = bits;  // ReLU mask bits, as the GEMM epilogue writes them
+  }
+}
+
+// ---------------------------------------------------------------------------
 // MaxPool
 // ---------------------------------------------------------------------------
 // Row-blocked launches: blockIdx.y = b * H + h (one output row for the forward,
@@ -1013,6 +1088,34 @@ extern "C" int wap_bias_grad(const float* dy, wap_layout_t l, float* db, float* 
   bias_grad_final<<<(l.C + 3) / 4, 128, 0, STREAM(stream)>>>(work, chunks, l.ld, l.C, db);
   WAP_LAUNCH_CHECK();
   g_wap_launches.fetch_add(2, std::memory_order_relaxed);
+  return WAP_OK;
+}
+
+extern "C" int wap_conv_direct(const float* x, wap_layout_t xl, const float* w, int k, int padding, int ldw,
+                               const float* bias, int relu, float* y, wap_layout_t yl, uint32_t* mbits,
+                               int64_t mbits_ld, void* stream) {
+  int rc;
+  if ((rc = check_layout(xl, "x")) || (rc = check_layout(yl, "y"))) return rc;
+  WAP_CHECK_ARG(x && w && y && k >= 1 && padding >= 0, "conv_direct: bad arguments");
+  WAP_CHECK_ARG(xl.ld == 4 && xl.C <= 4, "conv_direct: input must be one float4 per pixel (C <= 4)");
+  WAP_CHECK_ARG(yl.C % 32 == 0 && yl.ld % 4 == 0 && ldw >= yl.C, "conv_direct: Co must be a multiple of 32");
+  WAP_CHECK_ARG(yl.H == xl.H + 2 * padding - k + 1 && yl.W == xl.W + 2 * padding - k + 1 && yl.B == xl.B,
+                "conv_direct: output shape mismatch (stride-1 conv)");
+  const int64_t npix = (int64_t)yl.B * yl.H * yl.W;
+  WAP_CHECK_ARG(npix < (1LL << 31), "conv_direct: too many pixels");
+  const int smem = (k * k * xl.C + 1) * 32 * 4;
+  WAP_CHECK_ARG(smem <= 48 * 1024, "conv_direct: filter too large");
+  int64_t bx = (npix + 255) / 256;
+  if (bx > (int64_t)WAP_NUM_SMS * 16) bx = (int64_t)WAP_NUM_SMS * 16;
+  const dim3 grid((unsigned)bx, (unsigned)(yl.C / 32));
+  if (k == 3 && xl.C == 3)
+    conv_direct_kernel<3, 3><<<grid, 256, smem, STREAM(stream)>>>(x, xl, w, k, padding, ldw, bias, relu, y, yl, mbits,
+                                                                mbits_ld);
+  else
+    conv_direct_kernel<0, 0><<<grid, 256, smem, STREAM(stream)>>>(x, xl, w, k, padding, ldw, bias, relu, y, yl, mbits,
+                                                                mbits_ld);
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
   return WAP_OK;
 }
 

@@ -226,7 +226,14 @@ class Program:
                 s, p = conv_geometry(n, k)
                 ci = self.dims(n.inputs[0])[3]
                 ok = s == 1 and p == k // 2 and k % 2 == 1 and ci % 32 == 0 and k * k <= SHIFTED_MAX_TAPS
-                self.strategy[nid] = "shifted" if ok else ("s2d" if self._s2d_geometry(n) else "im2col")
+                if ok:
+                    self.strategy[nid] = "shifted"
+                elif self._s2d_geometry(n):
+                    self.strategy[nid] = "s2d"
+                elif self._direct_ok(n):
+                    self.strategy[nid] = "direct"
+                else:
+                    self.strategy[nid] = "im2col"
         # forward epilogue fusion: producer -> (bias node | None, relu node | None)
         self.fwd_fuse: dict[str, tuple[str | None, str | None]] = {}
         self.virtual: set[str] = set()
@@ -310,6 +317,17 @@ class Program:
                              self.mask_src(self.node(self.bwd_mask[g]).inputs[0]) == self.mask_src(x_id)
                              for g in grads):
                 self.pool_relu_fused.add(pool)
+
+    def _direct_ok(self, n: Node) -> bool:
+        """First-layer stride-1 conv over a <=4-channel graph input (one float4 per
+        pixel): computed directly on CUDA cores (wap_conv_direct), no im2col GEMM."""
+        if self.kind(n.inputs[0]) is not OpKind.INPUT or os.environ.get("WAP_NO_DIRECT"):
+            return False
+        k = self.dims(n.inputs[1])[0]
+        s, p = conv_geometry(n, k)
+        ci = self.dims(n.inputs[0])[3]
+        co = self.dims(n.id)[3]
+        return s == 1 and ci <= 4 and co % 32 == 0 and k * k * ci * 32 * 4 <= 48 * 1024
 
     def _s2d_geometry(self, n: Node):
         """Space-to-depth plan of a strided conv over a graph input (first layer, no
@@ -819,6 +837,16 @@ class Program:
         bias = self._in(self.node(zb), self.node(zb).inputs[1]) if zb is not None else None
         relu = r is not None
         b, ho, wo, _ = self.dims(n.id)
+        if self.strategy[n.id] == "direct":
+            if x.ld != 4:
+                raise EvalError(f"{n.id!r}: direct conv needs the input packed as one float4 per pixel")
+            bits = self._bits_alloc(out_id) if out_id in self.bits_src else None
+            self._emit(n.id, self.L.wap_conv_direct,
+                       (x.ptr, x.layout(), w.ptr, kk, p, w.ld, bias.ptr if bias is not None else None,
+                        1 if relu else 0, y.ptr, y.layout(), bits.data_ptr() if bits is not None else None,
+                        bits.ld_words if bits is not None else 0), "Conv2D (direct, CUDA cores)",
+                       alg_bytes=self._nbytes(x, y), keep=[bits] if bits is not None else None)
+            return
         if self.strategy[n.id] == "s2d":
             s_, p_, ks, hs, ws, ldc, halo = self._s2d_geometry(n)
             if y.pad != halo:
@@ -1036,6 +1064,19 @@ class Program:
             bo = N.operand(dy.ptr, inner=co, outer=dy.rows, ld=dy.ld, mn_major=True)
             self._gemm(n.id, kk * kk * ci, co, x.rows, a, bo, dw)
         else:
+            if self.strategy[conv] == "direct":
+                # the forward never built columns: im2col here, on the weight-gradient stream
+                cn = self.node(conv)
+                x_in = self._in(cn, cn.inputs[0])
+                s_, p_ = conv_geometry(cn, kk)
+                _, ho, wo, _ = self.dims(conv)
+                K = kk * kk * ci
+                ldcol = _ceil4(K)
+                colb = self.torch.empty(dy.rows * ldcol, dtype=self.torch.float32, device=self.device)
+                self.t[f"{conv}::col"] = Tensor((dy.rows, K), 0, ldcol, colb, "mat")
+                self._emit(n.id + "/im2col", self.L.wap_im2col,
+                           (x_in.ptr, x_in.layout(), kk, s_, p_, ho, wo, dy.pad, colb.data_ptr(), ldcol),
+                           "im2col (weight gradient)", alg_bytes=self._nbytes(x_in) + 4 * dy.rows * K)
             col = self.t[f"{conv}::col"]
             K = kk * kk * ci
             assert col.rows == dy.rows, (n.id, col.rows, dy.rows)
