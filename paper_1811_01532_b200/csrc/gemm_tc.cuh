@@ -108,11 +108,20 @@ struct Cfg {
 #define WAP_MAX_A_SLOTS 8
 #endif
   // Splitter groups take alternate k-steps and wait on stage / A-slot mbarriers by
-  // parity. A group must observe every phase of each barrier it waits on: with an
-  // odd ring size it would use a barrier only every other phase and a parity wait
-  // could pass on the phase before the one it needs (ABA). So both rings are a
-  // multiple of kSplitGroups (each group then owns a fixed subset of slots).
-  static constexpr int ring_round(int n) { return PREC == 3 ? n / kSplitGroups * kSplitGroups : n; }
+  // parity, so a group must observe every phase of each barrier it waits on (with an
+  // odd ring a group would otherwise meet a barrier only every other phase and a
+  // parity wait could pass on the phase before the one it needs: ABA). With
+  // WAP_RING_EVEN (default) the rings are rounded to a multiple of kSplitGroups
+  // (each group owns fixed slots); with WAP_RING_EVEN=0 a group instead also waits,
+  // without working, on the barriers of the other group's steps (splitter loop).
+  // Both pass the hang hunts (tools/gemm_loop.py, tools/hang_hunt.py); even rings
+  // measured slightly faster on VGG-16.
+#ifndef WAP_RING_EVEN
+#define WAP_RING_EVEN 1
+#endif
+  static constexpr int ring_round(int n) {
+    return (PREC == 3 && WAP_RING_EVEN) ? n / kSplitGroups * kSplitGroups : n;
+  }
   static constexpr int A_SLOTS =
       PREC == 3 ? ring_round(TMEM_A_SLOTS > WAP_MAX_A_SLOTS ? WAP_MAX_A_SLOTS : TMEM_A_SLOTS) : 1;
   static constexpr int STAGES = WIN ? 6 : ring_round(STAGES_SMEM > 8 ? 8 : STAGES_SMEM);
@@ -120,7 +129,7 @@ struct Cfg {
   static constexpr int THREADS = PREC == 3 ? 256 + 256 * kSplitGroups : 256;  // + splitter warp groups
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + kEpiStage + kBarBytes;
   static_assert(STAGES >= 2, "need at least two pipeline stages");
-  static_assert(PREC != 3 || (STAGES % kSplitGroups == 0 && A_SLOTS % kSplitGroups == 0 && A_SLOTS >= 1),
+  static_assert(PREC != 3 || !WAP_RING_EVEN || (STAGES % kSplitGroups == 0 && A_SLOTS % kSplitGroups == 0),
                 "3xTF32 rings must be multiples of the splitter group count");
   static_assert(B_ROWS % 32 == 0, "B rows per CTA must be a multiple of 32");
 };
@@ -1023,6 +1032,12 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           last_in_win = (tap == ntaps - 1) || (kc == tc.kc_end - 1);
         }
         if ((it % kSplitGroups) != group) {
+          // observe this step's stage / A-slot phases (no work) so that the parity
+          // waits of this group's own later steps never skip a phase
+          if (!WAP_RING_EVEN && (STAGES % kSplitGroups != 0 || C::A_SLOTS % kSplitGroups != 0)) {
+            mbar_wait(smem_u32(&full_bar[s]), ph);
+            mbar_wait(smem_u32(&aslot_bar[it % C::A_SLOTS]), ((it / C::A_SLOTS) & 1) ^ 1);
+          }
           // this group's own steps of the window are done (each ended in a named barrier)
           if (WIN && last_in_win && gt == 0) mbar_arrive(smem_u32(&wempty_bar[wslot]));
           if (++s == STAGES) { s = 0; ph ^= 1; }
