@@ -192,6 +192,7 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
   p->win = g.win_boxes > 0 ? 1 : 0;
   g.partial = nullptr;
   g.split_stride = d.M * d.ldc;
+  g.l2_prefetch = (d.M <= 512 && !getenv("WAP_NO_L2_PREFETCH")) ? 4 : 0;
   g.mbits_out = d.mbits_out;
   g.mbits_out_ld = d.mbits_out_ld;
   g.mbits_in = d.mbits_in;

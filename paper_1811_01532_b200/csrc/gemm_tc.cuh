@@ -76,6 +76,7 @@ struct GemmArgs {
   int64_t mbits_out_ld;
   const uint32_t* mbits_in;        // GradReLU mask bits (replaces `mask`)
   int64_t mbits_in_ld;
+  int32_t l2_prefetch;             // k-steps of TMA L2 prefetch ahead of the ring (0 = off)
 };
 
 // 3xTF32 keeps the A operand in TMEM (tcgen05 "TS" form): the splitter warps
@@ -327,6 +328,13 @@ __device__ __forceinline__ float4 ld_shared_v4f(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
   return v;
+}
+
+// TMA tile prefetch into L2 (no shared-memory destination, no completion tracking)
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* tm, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(tm)),
+               "r"(c0), "r"(c1)
+               : "memory");
 }
 
 // TMA store smem -> global (bulk group), completion tracked per issuing thread
@@ -646,6 +654,29 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           } else {
             mbar_arrive_expect_tx(fb, C::A_BYTES + C::B_BYTES);
             TW(3, issue(std::integral_constant<int, 1>{}));
+          }
+          // L2 prefetch g.l2_prefetch k-steps ahead of the smem ring for operands without
+          // filter taps: deepens the bytes in flight of streamed weights in small-M (FC)
+          // GEMMs beyond what the shared-memory stages hold (host enables it for M <= 512;
+          // for large-M wgrads it measured slower)
+          if (g.l2_prefetch > 0 && (kc + g.l2_prefetch) < tc.kc_end) {
+            const int kp = k + g.l2_prefetch * BK;
+            if (tpb == 0) {
+              if constexpr (B_MN) {
+#pragma unroll
+                for (int j = 0; j < NB; ++j) tma_prefetch_l2(&tmB, bc0[j], kp + bo[j]);
+              } else {
+                tma_prefetch_l2(&tmB, kp, b_row);
+              }
+            }
+            if (tpa == 0) {
+              if constexpr (A_MN) {
+#pragma unroll
+                for (int j = 0; j < NA; ++j) tma_prefetch_l2(&tmA, ac0[j], kp + ao[j]);
+              } else {
+                tma_prefetch_l2(&tmA, kp, a_row);
+              }
+            }
           }
           if (++s == STAGES) { s = 0; ph ^= 1; }
           k += BK;
