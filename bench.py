@@ -282,7 +282,7 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "fp32", "data": "synthetic (N(0,1) NHWC images, one-hot labels, He-scaled random-init weights)",
             "impl": "ours",
             "config": {"workload": f"{args.model} fp32 training, batch {b}/GPU, 224x224x3 synthetic ImageNet shape",
-                       "model": args.model, "global_batch": G, "batch_per_gpu": b, "image": 224,
+                       "network": args.model, "global_batch": G, "batch_per_gpu": b, "image": 224,
                        "parallelism": f"dp{world} replicated-variables (WAP transform, forced d={world})",
                        "gemm_precision": "3xTF32 (fp32-accurate)" if args.precision == 3 else "TF32",
                        "cuda_graph": tr._captured, "l2": "per-step working set > 126 MB L2 (no flush needed)",
@@ -377,7 +377,7 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "ms_per_step": round(total * 1e3 / steps, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "fp64", "data": "synthetic", "impl": "reference",
             "config": {"workload": f"{args.model} fp32 training, batch {b}/GPU, 224x224x3 synthetic ImageNet shape",
-                       "model": args.model, "global_batch": b * world, "parallelism": "CPU (oracle port of wap.interp)",
+                       "network": args.model, "global_batch": b * world, "parallelism": "CPU (oracle port of wap.interp)",
                        "sample_batch": sample},
             "cpu_baseline": {**last, "value": round(v, 3)},
             "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
