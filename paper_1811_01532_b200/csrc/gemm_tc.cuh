@@ -42,6 +42,9 @@ constexpr int kSmemBudget = (220 - 16 * kEpiBufs) * 1024;  // + the epilogue sta
 // row-per-thread writes and the coalesced reads, and the TMA store's source format
 constexpr int kEpiStage = kEpiBufs * 4 * 32 * 128;
 constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap offsets of A, B [512,768)
+#ifndef WAP_N64_PAIR
+#define WAP_N64_PAIR 1
+#endif
 // fewest TMEM A slots (3xTF32) worth keeping two accumulators for
 #ifndef WAP_MIN_A_SLOTS
 #define WAP_MIN_A_SLOTS 4
@@ -100,8 +103,15 @@ struct Cfg {
   // PREC 3 smem stage: [A raw] | B raw | B small
   static constexpr int STAGE_BYTES = PREC == 3 ? (A_OFF + 2 * B_BYTES) : (A_BYTES + B_BYTES);
   // two accumulators (epilogue overlap) only if >= 4 A stages still fit in TMEM
-  static constexpr int ACC_BUFS = (PREC == 3 && 512 - 2 * BN < WAP_MIN_A_SLOTS * 64) ? 1 : 2;
-  static constexpr int A_COL0 = ACC_BUFS * BN;
+  // PAIR (3xTF32, N = 64, one CTA): a tcgen05 MMA with N <= 64 costs about as much as
+  // N = 108 (tools/mma_probe.cu: ~54 cycles vs 32 at full rate), so big*big and
+  // big*small run as ONE N = 128 MMA over the contiguous [B_raw | B_small] rows of the
+  // stage into a 128-column accumulator, and small*big as an N = 64 MMA into its
+  // first half; the epilogue adds the two halves. 2 MMAs per k-slice instead of 3.
+  static constexpr bool PAIR = PREC == 3 && BN == 64 && CG == 1 && WAP_N64_PAIR;
+  static constexpr int ACC_W = PAIR ? 128 : BN;  // TMEM columns per accumulator
+  static constexpr int ACC_BUFS = (PREC == 3 && 512 - 2 * ACC_W < WAP_MIN_A_SLOTS * 64) ? 1 : 2;
+  static constexpr int A_COL0 = ACC_BUFS * ACC_W;
   static constexpr int TMEM_A_SLOTS = PREC == 3 ? (512 - A_COL0) / 64 : 64;
   static constexpr int STAGES_SMEM = kSmemBudget / STAGE_BYTES;
   // smem stages (TMA prefetch depth) and TMEM A slots (split -> MMA) are separate rings
@@ -202,6 +212,15 @@ __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_
       "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
       "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
 }
 
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -703,7 +722,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         const TileCoord tc = decode_tile(g, t, BN, CG);
         TW(1, mbar_wait(smem_u32(&tempty_bar[acc]), acc_ph ^ 1));
         tc_fence_after();
-        const uint32_t dacc = tmem_base + acc * BN;
+        const uint32_t dacc = tmem_base + acc * C::ACC_W;
         for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc) {
           if constexpr (PREC == 3) TW(2, mbar_wait(smem_u32(&conv_bar[s]), ph));
           else TW(2, mbar_wait(smem_u32(&full_bar[s]), ph));
@@ -733,7 +752,12 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
             for (int kk = 0; kk < BK / 8; ++kk) {
               const uint64_t bd = bd0 + kk * kB;
               const uint32_t first = kk > 0 ? 1u : first0;
-              if constexpr (PREC == 3) {
+              if constexpr (C::PAIR) {
+                constexpr uint32_t idesc2 = make_idesc_tf32(BM, 128, false, B_MN);
+                const uint32_t a_big = a_big0 + kk * 8;
+                umma_ts_cg<CG>(dacc, a_big, bd, idesc2, first);            // A * [B | B_small]
+                umma_ts_cg<CG>(dacc, a_big + 32, bd, idesc, 1u);           // small * B
+              } else if constexpr (PREC == 3) {
                 const uint32_t a_big = a_big0 + kk * 8;
                 umma_ts_cg<CG>(dacc, a_big + 32, bd, idesc, first);        // small * B
                 umma_ts_cg<CG>(dacc, a_big, bsd0 + kk * kB, idesc, 1u);    // A * small
@@ -834,7 +858,19 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
       for (int cb = 0; cb < BN / 32; ++cb) {
         uint32_t v[32];
         EPI_T0();
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN + cb * 32, v);
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * C::ACC_W + cb * 32, v);
+        if constexpr (C::PAIR) {
+          // second half of the pair accumulator (A * B_small), 16 columns at a time
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t v2[16];
+            tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * C::ACC_W + 64 + cb * 32 + hh * 16, v2);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              v[hh * 16 + j] = __float_as_uint(__uint_as_float(v[hh * 16 + j]) + __uint_as_float(v2[j]));
+          }
+        }
         tmem_ld_wait();
         EPI_T(1);
         const int nb = tc.n0 + cb * 32;
