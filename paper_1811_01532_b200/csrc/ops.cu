@@ -561,46 +561,59 @@ __global__ void __launch_bounds__(256) maxpool_fwd_kernel(const float* __restric
   }
 }
 
+// Gather form (windows may overlap): dx[h, w] = sum over the windows containing
+// (h, w) whose argmax is (h, w) of dy. WIN / S as template constants turn the window
+// range arithmetic into shifts (AlexNet 3/2, VGG 2/2); 0 / 0 = runtime values.
+template <int WINT, int ST>
 __global__ void __launch_bounds__(256) maxpool_bwd_kernel(const uint8_t* __restrict__ arg,
-                                                          const float* __restrict__ dy, wap_layout_t yl, int win,
-                                                          int s, float* __restrict__ dx, wap_layout_t xl,
+                                                          const float* __restrict__ dy, wap_layout_t yl, int win_rt,
+                                                          int s_rt, float* __restrict__ dx, wap_layout_t xl,
                                                           const float* __restrict__ mask, wap_layout_t ml) {
+  const int win = WINT ? WINT : win_rt, s = ST ? ST : s_rt;
   const int c4n = xl.ld / 4;
+  const int64_t yrow_stride = (int64_t)(yl.W + yl.pad) * yl.ld;
   for (int row = blockIdx.y; row < xl.B * xl.H; row += gridDim.y) {
-  const int b = row / xl.H, h = row - (row / xl.H) * xl.H;
-  // windows (ho, wo) with ho*s <= h < ho*s + win
-  const int ho_lo = h >= win ? (h - win) / s + 1 : 0;
-  const int ho_hi = min(h / s, yl.H - 1);
-  const int per = xl.W * c4n;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < per; j += gridDim.x * blockDim.x) {
-    const int w = j / c4n;
-    const int c = (j - w * c4n) * 4;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    const int wo_lo = w >= win ? (w - win) / s + 1 : 0;
-    const int wo_hi = min(w / s, yl.W - 1);
-    for (int ho = ho_lo; ho <= ho_hi; ++ho)
-      for (int wo = wo_lo; wo <= wo_hi; ++wo) {
-        const int local = (h - ho * s) * win + (w - wo * s);
-        const int64_t yi = lidx(yl, b, ho, wo, c);
-        const uchar4 a4 = *reinterpret_cast<const uchar4*>(arg + yi);
-        const float4 g = __ldg(reinterpret_cast<const float4*>(dy + yi));
-        if (a4.x == local) acc[0] += g.x;
-        if (a4.y == local) acc[1] += g.y;
-        if (a4.z == local) acc[2] += g.z;
-        if (a4.w == local) acc[3] += g.w;
+    const int b = row / xl.H, h = row - (row / xl.H) * xl.H;
+    // windows (ho, wo) with ho*s <= h < ho*s + win
+    const int ho_lo = h >= win ? (h - win) / s + 1 : 0;
+    const int ho_hi = min(h / s, yl.H - 1);
+    const int64_t y0 = lidx(yl, b, ho_lo, 0, 0);  // start of pooled row ho_lo
+    float* dxrow = dx + lidx(xl, b, h, 0, 0);
+    const float* mrow = mask ? mask + lidx(ml, b, h, 0, 0) : nullptr;
+    const int per = xl.W * c4n;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < per; j += gridDim.x * blockDim.x) {
+      const int w = j / c4n;
+      const int c = (j - w * c4n) * 4;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int wo_lo = w >= win ? (w - win) / s + 1 : 0;
+      const int wo_hi = min(w / s, yl.W - 1);
+      int64_t yr = y0;
+      for (int ho = ho_lo; ho <= ho_hi; ++ho, yr += yrow_stride) {
+        const int lh = (h - ho * s) * win;
+        for (int wo = wo_lo; wo <= wo_hi; ++wo) {
+          const int local = lh + (w - wo * s);
+          const int64_t yi = yr + (int64_t)wo * yl.ld + c;
+          const uchar4 a4 = *reinterpret_cast<const uchar4*>(arg + yi);
+          const float4 g = __ldg(reinterpret_cast<const float4*>(dy + yi));
+          if (a4.x == local) acc.x += g.x;
+          if (a4.y == local) acc.y += g.y;
+          if (a4.z == local) acc.z += g.z;
+          if (a4.w == local) acc.w += g.w;
+        }
       }
-    if (mask) {
-      const float4 m = __ldg(reinterpret_cast<const float4*>(mask + lidx(ml, b, h, w, c)));
-      if (!(m.x > 0.f)) acc[0] = 0.f;
-      if (!(m.y > 0.f)) acc[1] = 0.f;
-      if (!(m.z > 0.f)) acc[2] = 0.f;
-      if (!(m.w > 0.f)) acc[3] = 0.f;
+      if (mrow) {
+        const float4 m = __ldg(reinterpret_cast<const float4*>(mrow + (int64_t)w * ml.ld + c));
+        if (!(m.x > 0.f)) acc.x = 0.f;
+        if (!(m.y > 0.f)) acc.y = 0.f;
+        if (!(m.z > 0.f)) acc.z = 0.f;
+        if (!(m.w > 0.f)) acc.w = 0.f;
+      }
+      if (c + 0 >= xl.C) acc.x = 0.f;
+      if (c + 1 >= xl.C) acc.y = 0.f;
+      if (c + 2 >= xl.C) acc.z = 0.f;
+      if (c + 3 >= xl.C) acc.w = 0.f;
+      *reinterpret_cast<float4*>(dxrow + (int64_t)w * xl.ld + c) = acc;
     }
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (c + t >= xl.C) acc[t] = 0.f;
-    *reinterpret_cast<float4*>(dx + lidx(xl, b, h, w, c)) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-  }
   }
 }
 
@@ -1225,8 +1238,13 @@ extern "C" int wap_maxpool_bwd(const uint8_t* argmax, const float* dy, wap_layou
   WAP_CHECK_ARG(argmax != nullptr, "maxpool backward needs the forward argmax");
   WAP_CHECK_ARG(dxl.ld == dyl.ld, "maxpool: dx/dy ld mismatch");
   const int per = dxl.W * (dxl.ld / 4);
-  maxpool_bwd_kernel<<<pool_grid(dxl.B * dxl.H, per), 256, 0, STREAM(stream)>>>(argmax, dy, dyl, window, stride, dx,
-                                                                                 dxl, mask, ml);
+  const dim3 grid = pool_grid(dxl.B * dxl.H, per);
+  if (window == 3 && stride == 2)
+    maxpool_bwd_kernel<3, 2><<<grid, 256, 0, STREAM(stream)>>>(argmax, dy, dyl, window, stride, dx, dxl, mask, ml);
+  else if (window == 2 && stride == 2)
+    maxpool_bwd_kernel<2, 2><<<grid, 256, 0, STREAM(stream)>>>(argmax, dy, dyl, window, stride, dx, dxl, mask, ml);
+  else
+    maxpool_bwd_kernel<0, 0><<<grid, 256, 0, STREAM(stream)>>>(argmax, dy, dyl, window, stride, dx, dxl, mask, ml);
   WAP_LAUNCH_CHECK();
   COUNT_LAUNCH();
   return WAP_OK;
