@@ -379,6 +379,35 @@ __global__ void __launch_bounds__(256) s2d_input_kernel(const float* __restrict_
   }
 }
 
+// Compile-time stride / channels (AlexNet: s = 4, C = 3, x one float4 per pixel): one
+// thread per output float4 (16 per s2d pixel of ldc = 64: the pixel's 256 bytes are
+// written by 16 consecutive threads), source channel / pixel decode by constants.
+template <int S, int CC>
+__global__ void __launch_bounds__(256) s2d_input_const_kernel(const float* __restrict__ x, wap_layout_t xl, int p,
+                                                              int Hs, int Wsd, float* __restrict__ xs, int ldc) {
+  const uint32_t q4n = (uint32_t)ldc / 4;
+  const uint32_t total = (uint32_t)xl.B * Hs * Wsd * q4n;
+  const int64_t xrow = (int64_t)(xl.W + xl.pad) * xl.ld;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const uint32_t q = e % q4n, pix = e / q4n;
+    const uint32_t j = pix % (uint32_t)Wsd, r = pix / (uint32_t)Wsd;
+    const int ii = (int)(r % (uint32_t)Hs), b = (int)(r / (uint32_t)Hs);
+    const float* xb = x + lidx(xl, b, 0, 0, 0);
+    float o[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int cs = (int)q * 4 + l;
+      const int t = cs / CC, c = cs - t * CC;  // constant divisors
+      const int dy = t / S, dx = t - dy * S;
+      const int h = ii * S + dy - p, w = (int)j * S + dx - p;
+      o[l] = (cs < S * S * CC && h >= 0 && h < xl.H && w >= 0 && w < xl.W)
+                 ? __ldg(xb + h * xrow + (int64_t)w * xl.ld + c)
+                 : 0.f;
+    }
+    reinterpret_cast<float4*>(xs)[e] = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 // Narrow inputs (C <= 4 stored as one float4 per pixel, e.g. RGB padded to 4):
 // one thread per (s2d pixel, source pixel t = dy*s + dx) reads that pixel's float4
 // (coalesced along dx) and writes its C channels at t*C; threads t*C >= s*s*C
@@ -1142,7 +1171,9 @@ extern "C" int wap_s2d_input(const float* x, wap_layout_t xl, int stride, int pa
   WAP_CHECK_ARG(total4 < (1LL << 31), "s2d: grid too large for 32-bit indexing");
   int64_t blocks = (total4 + 255) / 256;
   if (blocks > (int64_t)WAP_NUM_SMS * 32) blocks = (int64_t)WAP_NUM_SMS * 32;
-  if (xl.ld == 4 && xl.C <= 4) {
+  if (stride == 4 && xl.C == 3 && xl.ld == 4) {
+    s2d_input_const_kernel<4, 3><<<(int)blocks, 256, 0, STREAM(stream)>>>(x, xl, padding, Hs, Ws, xs, ldc);
+  } else if (xl.ld == 4 && xl.C <= 4) {
     const int ss = stride * stride;
     const int64_t per = ldc / xl.C > ss ? (ldc + xl.C - 1) / xl.C : ss;
     const int64_t total = (int64_t)xl.B * Hs * Ws * per;
