@@ -417,11 +417,18 @@ def main():
         return
     import torch
 
+    # one rank per GPU; WAP_DIST_BACKEND=gloo (with ranks sharing GPUs) is only for
+    # exercising the multi-rank path on a single-GPU box
+    backend = os.environ.get("WAP_DIST_BACKEND", "nccl")
+    local_rank = local_rank % max(1, torch.cuda.device_count()) if backend != "nccl" else local_rank
     torch.cuda.set_device(local_rank)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     out, clocks = run_ours(args, rank, world, local_rank)
     if rank == 0:
         out["clocks"] = clocks
