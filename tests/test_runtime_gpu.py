@@ -68,6 +68,7 @@ REAL = [
     ("alexnet", dict(batch=2), 1),
     ("vgg16", dict(batch=2, image=32), 1),
     ("vgg16", dict(batch=4, image=32), 2),
+    ("alexnet", dict(batch=3, image=99), 3),  # a degree that is not a power of two
 ]
 
 
