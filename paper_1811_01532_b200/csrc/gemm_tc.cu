@@ -11,18 +11,35 @@ extern std::atomic<long long> g_wap_launches;
 
 namespace wapgemm {
 
+// Deterministic split-K reduction (slabs summed in split order) with the full
+// epilogue: bias, ReLU, GradReLU mask (float or bits), halo zeroing, and the
+// [out > 0] bits of the result. One warp per (row, 32-column chunk): lane j owns
+// column 32*chunk + j, so the mask-bit word of the chunk is one ballot.
 __global__ void splitk_reduce_kernel(const GemmArgs g, int splits) {
-  const int64_t total = g.M * g.N;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = i / g.N, n = i - m * g.N;
-    const float* p = g.partial + m * g.ldc + n;
-    float x = p[0];
-    for (int s = 1; s < splits; ++s) x += p[(int64_t)s * g.split_stride];
-    if (g.bias) x += g.bias[n];
-    if (g.relu) x = fmaxf(x, 0.f);
-    if (g.mask) x = (g.mask[m * g.ldm + n] > 0.f) ? x : 0.f;
-    if (halo_row(g, m)) x = 0.f;
-    g.c[m * g.ldc + n] = x;
+  const int lane = threadIdx.x & 31;
+  const int64_t nchunks = (g.N + 31) >> 5;
+  const int64_t tasks = g.M * nchunks;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < tasks; t += nwarps) {
+    const int64_t m = t / nchunks, chunk = t - m * nchunks;
+    const int64_t n = chunk * 32 + lane;
+    const bool valid = n < g.N;
+    float x = 0.f;
+    if (valid) {
+      const float* p = g.partial + m * g.ldc + n;
+      x = p[0];
+      for (int s = 1; s < splits; ++s) x += p[(int64_t)s * g.split_stride];
+      if (g.bias) x += g.bias[n];
+      if (g.relu) x = fmaxf(x, 0.f);
+      if (g.mbits_in) x = ((g.mbits_in[m * g.mbits_in_ld + chunk] >> lane) & 1u) ? x : 0.f;
+      else if (g.mask) x = (g.mask[m * g.ldm + n] > 0.f) ? x : 0.f;
+      if (halo_row(g, m)) x = 0.f;
+      g.c[m * g.ldc + n] = x;
+    }
+    if (g.mbits_out) {
+      const uint32_t bits = __ballot_sync(0xffffffffu, valid && x > 0.f);
+      if (lane == 0) g.mbits_out[m * g.mbits_out_ld + chunk] = bits;
+    }
   }
 }
 
@@ -96,10 +113,10 @@ Shape plan_shape(const wap_gemm_desc_t& d) {
   const long long tiles = (long long)s.m_tiles * s.n_tiles;
   const long long slots = WAP_NUM_SMS / s.cg;
   int splits = 1;
-  if (d.mbits_out || d.mbits_in) {
-    splits = 1;  // mask bits are produced / consumed by the non-split epilogue
-  } else if (d.splits > 0) {
-    splits = d.splits;
+  if (d.splits > 0) {
+    splits = d.splits;  // explicit (autotuned); split-K reduction handles mask bits too
+  } else if (d.mbits_out || d.mbits_in) {
+    splits = 1;  // automatic plans keep mask-bit GEMMs unsplit
   } else if (tiles < slots) {
     splits = (int)std::max(1LL, slots / tiles);
     splits = std::min(splits, std::max(1, s.k_chunks / 8));
@@ -197,7 +214,6 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
   g.mbits_out_ld = d.mbits_out_ld;
   g.mbits_in = d.mbits_in;
   g.mbits_in_ld = d.mbits_in_ld;
-  WAP_CHECK_ARG(!(d.mbits_out || d.mbits_in) || s.splits == 1, "ReLU mask bits need split-K off");
   // epilogue output through bulk tensor stores when C is TMA-addressable
   g.tma_store = 0;
   if (s.splits == 1 && (reinterpret_cast<uintptr_t>(d.c) & 15) == 0 && d.ldc % 4 == 0 &&
@@ -214,7 +230,8 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
   } else {
     p->tmC = p->tmA;  // unused
   }
-  WAP_CHECK_ARG(!(d.mbits_out || d.mbits_in) || g.tma_store, "ReLU mask bits need the TMA-store epilogue");
+  WAP_CHECK_ARG(!(d.mbits_out || d.mbits_in) || g.tma_store || s.splits > 1,
+                "ReLU mask bits need the TMA-store epilogue or split-K");
   if (s.splits > 1) {
     const int64_t need = (int64_t)s.splits * d.M * d.ldc * 4;
     WAP_CHECK_ARG(d.workspace != nullptr && d.workspace_bytes >= need,
@@ -238,9 +255,9 @@ int run_plan(const Plan& p, cudaStream_t st) {
   if (rc) return rc;
   g_wap_launches.fetch_add(1, std::memory_order_relaxed);
   if (p.splits > 1) {
-    const int64_t total = p.args.M * p.args.N;
+    const int64_t warps = p.args.M * ((p.args.N + 31) >> 5);
     const int threads = 256;
-    const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, WAP_NUM_SMS * 8);
+    const int blocks = (int)std::min<int64_t>((warps * 32 + threads - 1) / threads, WAP_NUM_SMS * 8);
     splitk_reduce_kernel<<<blocks, threads, 0, st>>>(p.args, p.splits);
     WAP_LAUNCH_CHECK();
     g_wap_launches.fetch_add(1, std::memory_order_relaxed);

@@ -114,7 +114,7 @@ def conv_fprop(xp, w, y, *, B, H, W, Ci, Co, k, pad, bias=None, relu=False, prec
     return call
 
 
-def conv_dgrad(dyp, w, dxp, *, B, H, W, Ci, Co, k, pad, mask=None, precision=3, run=True,
+def conv_dgrad(dyp, w, dxp, *, B, H, W, Ci, Co, k, pad, mask=None, precision=3, splits=0, run=True,
                stream=None):
     """dx_pad = GradConv2DX(dy_pad, w) (* [mask > 0]); dy halo must be zero."""
     hp, wp = H + pad, W + pad
@@ -125,7 +125,7 @@ def conv_dgrad(dyp, w, dxp, *, B, H, W, Ci, Co, k, pad, mask=None, precision=3, 
     bo = N.operand(w, inner=Co, outer=k * k * Ci, ld=Co, mn_major=False, tap_period=Co,
                    offsets=tuple(t * Ci for t in range(k * k)))
     d = _desc(rows, k * k * Co, Ci, ao, bo, dxp, Ci, mask=mask, ldm=(Ci if mask is not None else 0),
-              halo=(pad, H, W), precision=precision)
+              halo=(pad, H, W), precision=precision, splits=splits)
     call = GemmCall(d, device=dxp.device)
     if run:
         call(stream)

@@ -693,19 +693,28 @@ class Program:
             # BN = 128 keeps two TMEM accumulators in 3xTF32 (epilogue overlaps the next tile),
             # wider tiles halve B traffic: measure both where N allows
             bns = (0, 128) if (self.precision == 3 and st.desc.N >= 192) else (0,)
-            for cluster, window, bn in [(c, w, b) for c in (1, 2) for w in windows for b in bns]:
+            # explicit split-K against wave quantization (WAP_AUTOTUNE_SPLITK=1): a GEMM of
+            # only a few waves of output tiles (e.g. 13x13 convs: 98 CTA-pair tiles on 74
+            # pairs) also tries 2-4 K slabs. Off by default: measured on B200 (r01), no
+            # AlexNet / VGG-16 GEMM got faster (slab traffic + reduce > the tail wave)
+            few_waves = (-(-st.desc.M // 128)) * (-(-st.desc.N // 256)) < 4 * 148
+            auto_split = self.L.wap_gemm_workspace_bytes(C.byref(st.desc)) > 0
+            k_chunks = -(-st.desc.K // 32)
+            splits_opts = (0,) + tuple(x for x in (2, 3, 4) if few_waves and not auto_split
+                                       and st.desc.splits == 0 and k_chunks >= 16 * x
+                                       and os.environ.get("WAP_AUTOTUNE_SPLITK", "0") == "1")
+            for cluster, window, bn, sp in [(c, w, b, x) for c in (1, 2) for w in windows for b in bns
+                                            for x in splits_opts]:
                 d = type(st.desc).from_buffer_copy(st.desc)
                 d.cluster = cluster
                 d.window = window
                 d.block_n = bn
+                d.splits = sp if sp else st.desc.splits
                 d.workspace, d.workspace_bytes = None, 0
                 try:
                     call = GemmCall(d, device=self.device)
                 except Exception:
                     continue
-                if os.environ.get("WAP_AUTOTUNE_LOG"):
-                    print(f"autotune {st.name} M={d.M} N={d.N} K={d.K} cluster={cluster} window={window} bn={bn}",
-                          flush=True)
                 N.check(self.L.wap_gemm_plan_run(call._plan, s), "autotune warm-up")
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -714,6 +723,9 @@ class Program:
                 e1.record(stream)
                 e1.synchronize()
                 ms = e0.elapsed_time(e1) / reps
+                if os.environ.get("WAP_AUTOTUNE_LOG"):
+                    print(f"autotune {st.name} M={d.M} N={d.N} K={d.K} cluster={cluster} window={window} bn={bn} "
+                          f"splits={sp} {ms:.4f} ms", flush=True)
                 if best_ms is None or ms < best_ms:
                     best, best_ms = call, ms
             st.call = best

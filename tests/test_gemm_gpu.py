@@ -108,3 +108,61 @@ def test_conv_shifted(cuda, prec, Bn, H, Ci, Co, k):
     assert dev(dxp[:, :H, :W], ref_dx) < TOL[prec]
     assert dxp[:, H:].abs().max().item() == 0 and dxp[:, :, W:].abs().max().item() == 0
     assert dev(dw, ref_dw) < TOL[prec]
+
+
+def _pack_bits(v):
+    """[rows, n] bool -> [rows, ceil(n/32)] int32 words, bit j = column 32*w + j."""
+    rows, n = v.shape
+    ldw = (n + 31) // 32
+    vb = torch.zeros(rows, ldw * 32, dtype=torch.int64, device=v.device)
+    vb[:, :n] = v.to(torch.int64)
+    words = (vb.view(rows, ldw, 32) << torch.arange(32, device=v.device)).sum(-1)
+    return torch.where(words >= 2**31, words - 2**32, words).to(torch.int32)
+
+
+@pytest.mark.parametrize("splits", [0, 2, 3])
+@pytest.mark.parametrize("Co", [96, 72])
+def test_conv_mask_bits_splitk(cuda, splits, Co):
+    """ReLU mask bits published by a conv fprop and consumed by a dgrad, through the
+    fused TMA-store epilogue (splits=0) and the split-K reduction (explicit splits)."""
+    Bn, H, Ci, k = 2, 13, 64, 3
+    W, p = H, 1
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(Bn, H, W, Ci, device=cuda, generator=g)
+    w = torch.randn(k, k, Ci, Co, device=cuda, generator=g) * 0.1
+    bias = torch.randn(Co, device=cuda, generator=g)
+    xp = _pad(x, p)
+    rows = Bn * (H + p) * (W + p)
+    yp = torch.full((Bn, H + p, W + p, Co), float("nan"), device=cuda)
+    bits = torch.full((rows, (Co + 31) // 32), -7, dtype=torch.int32, device=cuda)
+    d = K.conv_fprop(xp, w, yp, B=Bn, H=H, W=W, Ci=Ci, Co=Co, k=k, pad=p, bias=bias, relu=True,
+                     run=False).desc
+    d.mbits_out, d.mbits_out_ld, d.splits = bits.data_ptr(), bits.shape[1], splits
+    d.workspace, d.workspace_bytes = None, 0
+    K.GemmCall(d, device=cuda)()
+    torch.cuda.synchronize()
+    ref = F.conv2d(x.double().permute(0, 3, 1, 2), w.double().permute(3, 2, 0, 1), bias.double(), padding=p)
+    assert dev(yp[:, :H, :W], torch.relu(ref).permute(0, 2, 3, 1)) < TOL[3]
+    assert torch.equal(bits, _pack_bits(yp.reshape(rows, Co) > 0))
+
+    if Co % 32:
+        return  # a dgrad's K chunks must not straddle taps (tap_period = Co, multiple of 32)
+    # dgrad of a conv whose input passed a ReLU: GradReLU from bits == from the float mask
+    dy = torch.randn(Bn, H, W, Co, device=cuda, generator=g)
+    dyp = _pad(dy, p)
+    xbits = _pack_bits(xp.reshape(rows, Ci) > 0)
+    dx_f = torch.full_like(xp, float("nan"))
+    K.conv_dgrad(dyp, w, dx_f, B=Bn, H=H, W=W, Ci=Ci, Co=Co, k=k, pad=p, mask=xp, splits=splits)
+    dx_b = torch.full_like(xp, float("nan"))
+    d = K.conv_dgrad(dyp, w, dx_b, B=Bn, H=H, W=W, Ci=Ci, Co=Co, k=k, pad=p, splits=splits, run=False).desc
+    d.mbits_in, d.mbits_in_ld = xbits.data_ptr(), xbits.shape[1]
+    d.workspace, d.workspace_bytes = None, 0
+    K.GemmCall(d, device=cuda)()
+    torch.cuda.synchronize()
+    if splits:  # same K slabs, same order: bitwise equal
+        assert torch.equal(dx_b, dx_f)
+    xd = x.double().permute(0, 3, 1, 2).requires_grad_(True)
+    F.conv2d(xd, w.double().permute(3, 2, 0, 1), padding=p).backward(dy.double().permute(0, 3, 1, 2))
+    ref_dx = (xd.grad * (xd > 0)).permute(0, 2, 3, 1)
+    assert dev(dx_b[:, :H, :W], ref_dx) < TOL[3] and dev(dx_f[:, :H, :W], ref_dx) < TOL[3]
+    assert dx_b[:, H:].abs().max().item() == 0 and dx_b[:, :, W:].abs().max().item() == 0
