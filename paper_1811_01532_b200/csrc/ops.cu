@@ -646,6 +646,90 @@ __global__ void __launch_bounds__(256) maxpool_bwd_kernel(const uint8_t* __restr
   }
 }
 
+// Stride-2 patch form (AlexNet 3/2, VGG 2/2): one thread owns a 2x2 block of input
+// pixels x 4 channels. For s = 2 that block lies in at most (WIN-1)^2 windows
+// (ho in {i-1, i} x wo in {j-1, j} for WIN 3; just (i, j) for WIN 2), so each
+// pooled (argmax, dy) pair is loaded once per block instead of once per pixel it
+// covers (9 -> 4 loads per 4 pixels for 3/2), and the window-relative offsets are
+// compile-time. Windows are visited in the per-pixel gather's order (ho, then wo
+// ascending), so every dx element is the same float sum, bit for bit.
+template <int WIN>
+__global__ void __launch_bounds__(256) maxpool_bwd_s2_kernel(const uint8_t* __restrict__ arg,
+                                                             const float* __restrict__ dy, wap_layout_t yl,
+                                                             float* __restrict__ dx, wap_layout_t xl,
+                                                             const float* __restrict__ mask, wap_layout_t ml) {
+  constexpr int NW = WIN - 1;  // windows per axis covering a 2-pixel span
+  const int c4n = xl.ld / 4;
+  const int PH = (xl.H + 1) >> 1, PW = (xl.W + 1) >> 1;
+  const int per = PW * c4n;
+  const int64_t xrs = (int64_t)(xl.W + xl.pad) * xl.ld;
+  const int64_t mrs = (int64_t)(ml.W + ml.pad) * ml.ld;
+  for (int prow = blockIdx.y; prow < xl.B * PH; prow += gridDim.y) {
+    const int b = prow / PH, i = prow - b * PH;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < per; j += gridDim.x * blockDim.x) {
+      const int jj = j / c4n;
+      const int c = (j - jj * c4n) * 4;
+      float4 acc[2][2];
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) acc[p][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int a = 0; a < NW; ++a) {
+        const int ho = i - (NW - 1) + a;
+        if (ho < 0 || ho >= yl.H) continue;
+#pragma unroll
+        for (int bb = 0; bb < NW; ++bb) {
+          const int wo = jj - (NW - 1) + bb;
+          if (wo < 0 || wo >= yl.W) continue;
+          const int64_t yi = lidx(yl, b, ho, wo, c);
+          const uchar4 a4 = *reinterpret_cast<const uchar4*>(arg + yi);
+          const float4 g = __ldg(reinterpret_cast<const float4*>(dy + yi));
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            const int r = 2 * (NW - 1 - a) + p;  // row of pixel (2i+p) inside window ho
+            if (r >= WIN) continue;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int cc = 2 * (NW - 1 - bb) + q;
+              if (cc >= WIN) continue;
+              const int local = r * WIN + cc;
+              if (a4.x == local) acc[p][q].x += g.x;
+              if (a4.y == local) acc[p][q].y += g.y;
+              if (a4.z == local) acc[p][q].z += g.z;
+              if (a4.w == local) acc[p][q].w += g.w;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const int h = 2 * i + p;
+        if (h >= xl.H) continue;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int w = 2 * jj + q;
+          if (w >= xl.W) continue;
+          float4 v = acc[p][q];
+          if (mask) {
+            const float4 m = __ldg(reinterpret_cast<const float4*>(mask + b * (int64_t)(ml.H + ml.pad) * mrs +
+                                                                   h * mrs + (int64_t)w * ml.ld + c));
+            if (!(m.x > 0.f)) v.x = 0.f;
+            if (!(m.y > 0.f)) v.y = 0.f;
+            if (!(m.z > 0.f)) v.z = 0.f;
+            if (!(m.w > 0.f)) v.w = 0.f;
+          }
+          if (c + 0 >= xl.C) v.x = 0.f;
+          if (c + 1 >= xl.C) v.y = 0.f;
+          if (c + 2 >= xl.C) v.z = 0.f;
+          if (c + 3 >= xl.C) v.w = 0.f;
+          *reinterpret_cast<float4*>(dx + b * (int64_t)(xl.H + xl.pad) * xrs + h * xrs + (int64_t)w * xl.ld + c) = v;
+        }
+      }
+    }
+  }
+}
+
 // rows beyond gridDim.y's 65535 limit are covered by the kernels' row loop
 dim3 pool_grid(int rows, int per) {
   return dim3((unsigned)std::max(1, std::min((per + 255) / 256, 64)), (unsigned)std::min(rows, 65535));
@@ -1270,7 +1354,14 @@ extern "C" int wap_maxpool_bwd(const uint8_t* argmax, const float* dy, wap_layou
   WAP_CHECK_ARG(dxl.ld == dyl.ld, "maxpool: dx/dy ld mismatch");
   const int per = dxl.W * (dxl.ld / 4);
   const dim3 grid = pool_grid(dxl.B * dxl.H, per);
-  if (window == 3 && stride == 2)
+  const bool pixel_form = getenv("WAP_POOL_BWD_PIXEL") != nullptr;  // A/B switch: per-pixel gather
+  if (stride == 2 && (window == 3 || window == 2) && !pixel_form) {
+    const dim3 g2 = pool_grid(dxl.B * ((dxl.H + 1) / 2), ((dxl.W + 1) / 2) * (dxl.ld / 4));
+    if (window == 3)
+      maxpool_bwd_s2_kernel<3><<<g2, 256, 0, STREAM(stream)>>>(argmax, dy, dyl, dx, dxl, mask, ml);
+    else
+      maxpool_bwd_s2_kernel<2><<<g2, 256, 0, STREAM(stream)>>>(argmax, dy, dyl, dx, dxl, mask, ml);
+  } else if (window == 3 && stride == 2)
     maxpool_bwd_kernel<3, 2><<<grid, 256, 0, STREAM(stream)>>>(argmax, dy, dyl, window, stride, dx, dxl, mask, ml);
   else if (window == 2 && stride == 2)
     maxpool_bwd_kernel<2, 2><<<grid, 256, 0, STREAM(stream)>>>(argmax, dy, dyl, window, stride, dx, dxl, mask, ml);

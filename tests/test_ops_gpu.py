@@ -1,0 +1,74 @@
+"""HBM-bound op kernels through the C ABI vs torch fp64 (GPU).
+
+MaxPool backward (interp rules in oracle/interp_ref.py; first-max ties): the
+stride-2 patch kernel must equal the per-pixel gather kernel bit for bit (same
+window order) and torch's max_pool2d backward on tie-free data."""
+
+import os
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_1811_01532_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+
+def _buf(B, H, W, ld, pad, cuda, fill=float("nan")):
+    return torch.full((B, H + pad, W + pad, ld), fill, device=cuda)
+
+
+def _pool_bwd(L, arg, dy, yl, win, s, dx, xl, mask, ml, pixel: bool):
+    if pixel:
+        os.environ["WAP_POOL_BWD_PIXEL"] = "1"
+    try:
+        N.check(L.wap_maxpool_bwd(arg.data_ptr(), dy.data_ptr(), yl, win, s, dx.data_ptr(), xl,
+                                  mask.data_ptr() if mask is not None else None, ml, None))
+    finally:
+        os.environ.pop("WAP_POOL_BWD_PIXEL", None)
+
+
+@pytest.mark.parametrize("B,H,C,ld,win,pad,use_mask", [
+    (2, 55, 64, 64, 3, 0, False),   # AlexNet pool1
+    (2, 27, 192, 192, 3, 2, True),  # AlexNet pool2 (trailing halo on the input), float mask
+    (3, 13, 6, 8, 3, 1, False),     # padded channel lanes
+    (2, 56, 64, 64, 3, 0, False),   # last input row in no window
+    (2, 28, 128, 128, 2, 1, False),  # VGG 2/2
+    (1, 15, 4, 4, 2, 0, True),      # odd extent: last row / column uncovered
+])
+def test_maxpool_bwd_patch_matches_gather_and_torch(cuda, B, H, C, ld, win, pad, use_mask):
+    L = N.lib()
+    W, s = H, 2
+    Ho = (H - win) // s + 1
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = _buf(B, H, W, ld, pad, cuda, 0.0)
+    x[:, :H, :W, :C] = torch.randn(B, H, W, C, device=cuda, generator=g)
+    xl = N.wap_layout_t(B, H, W, C, pad, ld)
+    yl = N.wap_layout_t(B, Ho, Ho, C, 0, ld)
+    y = _buf(B, Ho, Ho, ld, 0, cuda)
+    arg = torch.zeros(B * Ho * Ho * ld, dtype=torch.uint8, device=cuda)
+    N.check(L.wap_maxpool_fwd_ex(x.data_ptr(), xl, win, s, y.data_ptr(), yl, arg.data_ptr(), 0, None))
+    dy = _buf(B, Ho, Ho, ld, 0, cuda, 0.0)
+    dy[..., :C] = torch.randn(B, Ho, Ho, C, device=cuda, generator=g)
+    mask = ml = None
+    ml = xl
+    if use_mask:
+        mask = torch.randn(x.shape, device=cuda, generator=g)
+    dx_patch = _buf(B, H, W, ld, pad, cuda)
+    dx_pix = _buf(B, H, W, ld, pad, cuda)
+    _pool_bwd(L, arg, dy, yl, win, s, dx_patch, xl, mask, ml, pixel=False)
+    _pool_bwd(L, arg, dy, yl, win, s, dx_pix, xl, mask, ml, pixel=True)
+    torch.cuda.synchronize()
+    assert torch.equal(dx_patch[:, :H, :W], dx_pix[:, :H, :W])
+    # halo rows / columns are never written
+    if pad:
+        assert torch.isnan(dx_patch[:, H:]).all() and torch.isnan(dx_patch[:, :, W:]).all()
+    xd = x[:, :H, :W, :C].double().permute(0, 3, 1, 2).requires_grad_(True)
+    F.max_pool2d(xd, win, s).backward(dy[..., :C].double().permute(0, 3, 1, 2))
+    ref = xd.grad.permute(0, 2, 3, 1)
+    if use_mask:
+        ref = ref * (mask[:, :H, :W, :C] > 0)
+    got = dx_patch[:, :H, :W, :C].double()
+    assert (got - ref).abs().max().item() < 1e-6
+    assert (dx_patch[:, :H, :W, C:] == 0).all()
