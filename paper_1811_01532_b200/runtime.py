@@ -685,7 +685,10 @@ class Program:
         stream = torch.cuda.current_stream(self.device)
         s = N.stream_ptr()
         for st in self.steps + self.update_steps:
-            if not isinstance(st, _GemmStep) or st.desc.M <= 128:
+            if not isinstance(st, _GemmStep):
+                continue
+            small_m = st.desc.M <= 128
+            if small_m and os.environ.get("WAP_AUTOTUNE_FC", "1") == "0":
                 continue
             best, best_ms = st.call, None
             a = st.desc.a
@@ -703,8 +706,14 @@ class Program:
             splits_opts = (0,) + tuple(x for x in (2, 3, 4) if few_waves and not auto_split
                                        and st.desc.splits == 0 and k_chunks >= 16 * x
                                        and os.environ.get("WAP_AUTOTUNE_SPLITK", "0") == "1")
-            for cluster, window, bn, sp in [(c, w, b, x) for c in (1, 2) for w in windows for b in bns
-                                            for x in splits_opts]:
+            if small_m:
+                # FC layers (M = batch <= 128): a handful of output tiles, so the K split
+                # sets the grid; the automatic plan (<= one wave) vs ~2-4 waves of slabs
+                # (M x N slabs are small: e.g. 19 MB at fc6 x 9). Measured r01: BN = 128
+                # wins on every AlexNet FC GEMM (fc8 0.031 -> 0.024 ms), 9 slabs on fc6/fc7
+                splits_opts = (0,) + tuple(x for x in (9, 18) if k_chunks >= 8 * x)
+            for cluster, window, bn, sp in [(c, w, b, x) for c in ((1,) if small_m else (1, 2))
+                                            for w in windows for b in bns for x in splits_opts]:
                 d = type(st.desc).from_buffer_copy(st.desc)
                 d.cluster = cluster
                 d.window = window
