@@ -291,8 +291,9 @@ def run_ours(args, rank, world, local_rank):
                        "cuda_graph": tr._captured, "l2": "per-step working set > 126 MB L2 (no flush needed)",
                        "wau_choice_8gpu": wau8.d},
             "e2e": {"value": round(G / (e2e_ms / 1e3), 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "path": "Trainer.step_async: pinned H2D on a copy stream overlapping the previous step, "
-                            "pack + CUDA-graph step, async D2H of the loss",
+                    "path": "Trainer.step_async: pinned H2D into one of two staging slots on a copy stream "
+                            "(overlapping the previous step), then that slot's CUDA graph of [pack, the step, "
+                            "loss D2H into pinned memory]",
                     "d2h_bytes_per_step": 4, "host_ms_per_step": round(host_ms, 3), "loss": loss},
             "gpu_launches": launches * args.steps,
             "roofline": {"bound": "tensor", "kernel": dom.name, "gemm_shape_MNK": list(dom.shape),

@@ -1136,6 +1136,21 @@ __global__ void pack_kernel(const float* __restrict__ src, float* __restrict__ d
   }
 }
 
+// Image upload path (dense NHWC C=3 -> ld=4 layout): blockIdx.y = image row, one
+// pixel per thread: a warp reads 384 contiguous bytes (3 coalesced 4-byte loads per
+// lane) and writes 512 contiguous bytes (one float4 per lane, padding lane 0).
+// No per-pixel index division.
+__global__ void __launch_bounds__(256) pack_c3_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                                       wap_layout_t l) {
+  for (int row = blockIdx.y; row < l.B * l.H; row += gridDim.y) {
+    const int b = row / l.H, h = row - (row / l.H) * l.H;
+    const float* s = src + (int64_t)row * l.W * 3;
+    float4* d = reinterpret_cast<float4*>(dst + lidx(l, b, h, 0, 0));
+    for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < l.W; w += gridDim.x * blockDim.x)
+      d[w] = make_float4(__ldg(s + 3 * w), __ldg(s + 3 * w + 1), __ldg(s + 3 * w + 2), 0.f);
+  }
+}
+
 __global__ void sgd_kernel(const float* __restrict__ w, const float* __restrict__ g, float lr, float* __restrict__ o,
                            int64_t n) {
   const int64_t n4 = n / 4;
@@ -1423,6 +1438,9 @@ extern "C" int wap_pack(const float* dense, wap_layout_t l, float* dst, int unpa
   WAP_CHECK_ARG(l.B >= 1 && l.H >= 1 && l.W >= 1 && l.C >= 1 && l.ld >= l.C && l.pad >= 0, "pack: bad layout");
   const int64_t total = (int64_t)l.B * l.H * l.W * l.C;
   if (unpack) pack_kernel<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(dst, const_cast<float*>(dense), l, 1);
+  else if (l.C == 3 && l.ld == 4 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0)
+    pack_c3_kernel<<<dim3((unsigned)((l.W + 255) / 256), (unsigned)std::min(l.B * l.H, 65535)), 256, 0,
+                     STREAM(stream)>>>(dense, dst, l);
   else pack_kernel<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(dense, dst, l, 0);
   WAP_LAUNCH_CHECK();
   COUNT_LAUNCH();

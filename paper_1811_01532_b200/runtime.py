@@ -1241,7 +1241,70 @@ class Program:
                 st(N.stream_ptr(side))
         self.graph_exec = g
 
+    def capture_with(self, pre=(), post=()):
+        """One CUDA graph of `pre` callables + the whole step + `post` callables (each
+        called with the capture stream's pointer). No warm-up: capture() already ran
+        one, so kernels are loaded and GEMM plans tuned."""
+        torch = self.torch
+        if any(isinstance(s, _CollectiveStep) for s in self.steps):
+            raise EvalError("steps with cross-process collectives are not captured")
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            sp = N.stream_ptr(side)
+            for f in pre:
+                f(sp)
+            for st in self.steps:
+                st(sp)
+            for f in post:
+                f(sp)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        return g
+
     # ----------------------------------------------------------- host binding
+    def h2d_staged(self, values: dict, copy_stream, slot: int, after=None) -> dict:
+        """H2D of this step's shard into staging buffer `slot` on `copy_stream` (after
+        event `after`, the last reader of that slot); the compute stream waits for it.
+        Returns {input id: staging tensor}."""
+        torch = self.torch
+        staged = self.staging(values, slot)
+        if after is not None:
+            copy_stream.wait_event(after)
+        with torch.cuda.stream(copy_stream):
+            for k, v in values.items():
+                if isinstance(v, np.ndarray):
+                    v = torch.from_numpy(v)
+                if v.dtype != torch.float32:
+                    raise EvalError(f"binding {k!r} must be float32 for the async path")
+                staged[k].copy_(v.reshape(-1), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(copy_stream)
+        torch.cuda.current_stream(self.device).wait_event(ev)
+        return staged
+
+    def staging(self, values: dict, slot: int) -> dict:
+        """The dense device staging buffers of `slot` for the inputs in `values`."""
+        torch = self.torch
+        if not hasattr(self, "_stg2"):
+            self._stg2 = [{}, {}]
+        for k in values:
+            if k not in self._stg2[slot]:
+                n = int(np.prod(self.t[k].dims))
+                self._stg2[slot][k] = torch.empty(n, dtype=torch.float32, device=self.device)
+        return {k: self._stg2[slot][k] for k in values}
+
+    def pack_staged(self, staged: dict, stream_ptr) -> None:
+        """Staging -> input layouts (the step's first launches; capturable). Dense
+        inputs (labels) are a device copy on the current stream (the capture stream)."""
+        for k, st in staged.items():
+            t = self.t[k]
+            n = st.numel()
+            if t.pad == 0 and t.ld == t.dims[-1]:
+                t.buf[:n].copy_(st, non_blocking=True)
+            else:
+                N.check(self.L.wap_pack(st.data_ptr(), t.layout(), t.ptr, 0, stream_ptr), "pack")
+
     def input_ids(self) -> list[str]:
         return [nid for nid in self.order if self.kind(nid) is OpKind.INPUT]
 

@@ -72,3 +72,19 @@ def test_maxpool_bwd_patch_matches_gather_and_torch(cuda, B, H, C, ld, win, pad,
     got = dx_patch[:, :H, :W, :C].double()
     assert (got - ref).abs().max().item() < 1e-6
     assert (dx_patch[:, :H, :W, C:] == 0).all()
+
+
+@pytest.mark.parametrize("B,H,W,pad", [(3, 224, 224, 0), (2, 8, 12, 2), (2, 7, 9, 0)])
+def test_pack_images_c3(cuda, B, H, W, pad):
+    """wap_pack of dense NHWC C=3 images into the ld=4 layout (fast 4-pixel path when
+    W % 4 == 0, generic otherwise): exact copy, padding lane 0, halo untouched."""
+    L = N.lib()
+    src = torch.randn(B, H, W, 3, device=cuda)
+    dst = torch.full((B, H + pad, W + pad, 4), float("nan"), device=cuda)
+    dst[..., 3] = 0.0
+    N.check(L.wap_pack(src.data_ptr(), N.wap_layout_t(B, H, W, 3, pad, 4), dst.data_ptr(), 0, None))
+    torch.cuda.synchronize()
+    assert torch.equal(dst[:, :H, :W, :3], src)
+    assert (dst[:, :H, :W, 3] == 0).all()
+    if pad:
+        assert torch.isnan(dst[:, H:, :, :3]).all() and torch.isnan(dst[:, :, W:, :3]).all()

@@ -55,20 +55,22 @@ def test_trainer_graph_step_matches_execute(cuda, net, kw, monkeypatch):
 
 def test_step_async_matches_step(cuda, monkeypatch):
     """The overlapped input path (H2D on a copy stream, async loss D2H) computes the
-    same two consecutive steps as the synchronous Trainer.step (to fp32 rounding)."""
+    same three consecutive steps as the synchronous Trainer.step (to fp32 rounding)."""
     monkeypatch.setenv("WAP_AUTOTUNE", "0")
     g = models.MODELS["alexnet"](batch=4, image=99)
-    b1, b2 = _bindings(g, seed=11), _bindings(g, seed=12)
+    b1, b2, b3 = _bindings(g, seed=11), _bindings(g, seed=12), _bindings(g, seed=13)
     variables = {k: v for k, v in b1.items() if k not in ("images", "labels")}
     tp = trainer.plan_training(g, 1, planner.load_profile("b200"), force_d=1)
-    pinned = [{k: torch.from_numpy(b[k]).pin_memory() for k in ("images", "labels")} for b in (b1, b2)]
+    pinned = [{k: torch.from_numpy(b[k]).pin_memory() for k in ("images", "labels")} for b in (b1, b2, b3)]
     ta = trainer.Trainer(tp, variables=variables, use_graph=True)
     ta.step_async(pinned[0])
     ta.step_async(pinned[1])
+    ta.step_async(pinned[2])  # staging slot 0 and its graph again
     la = ta.last_loss()
     tb = trainer.Trainer(tp, variables=variables, use_graph=True)
     tb.step(pinned[0])
-    lb = tb.step(pinned[1], fetch=True)
+    tb.step(pinned[1])
+    lb = tb.step(pinned[2], fetch=True)
     # same default GEMM plans on both sides; agreement to rounding
     assert abs(la - lb) <= 1e-6 * max(1.0, abs(lb))
     va, vb = ta.variables(), tb.variables()
