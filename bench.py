@@ -123,7 +123,8 @@ class ClockSampler:
             if len(f) < 10:
                 continue
             try:
-                rows.append((self._stamp(f[0]), float(f[2]), float(f[3]), f[6:10]))
+                pw = float(f[4]) if f[4] not in ("", "[N/A]", "N/A") else float("nan")
+                rows.append((self._stamp(f[0]), float(f[2]), float(f[3]), f[6:10], pw))
             except ValueError:
                 continue
         sel = rows
@@ -134,9 +135,11 @@ class ClockSampler:
                 sel = inside
         reasons = {n for r in sel for n, v in zip(names, r[3]) if v.lower() == "active"}
         sm = [r[1] for r in sel]
+        pw = [r[4] for r in sel if r[4] == r[4]]
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": sel[-1][2] if sel else None,
                 "reasons": sorted(reasons), "samples": len(sm),
-                "window": "timed region" if sel is not rows else "whole run"}
+                "window": "timed region" if sel is not rows else "whole run",
+                "power_w": round(float(np.median(pw)), 1) if pw else None}
 
 
 def synthetic_batch(model_graph, rank: int, b: int, seed: int = 42):
@@ -323,7 +326,22 @@ def run_ours(args, rank, world, local_rank):
             # isolated autotune time of each GEMM (same launch, warm L2, no neighbours)
             out["gemm_tuned_ms"] = {k: round(v[1].tuned_ms, 4) for k, v in per.items()
                                     if getattr(v[1], "tuned_ms", None) is not None}
-    return out, clk.summary()
+    clocks = clk.summary()
+    # WAP's own model next to the measurement: Eq. (1) step time for
+    # this d (estimate_total; additive compute + allreduce, no overlap) and estimate_power
+    # (host + d * GPU power) against the measured step time and NVML board power
+    est = tplan.plan.chosen
+    pw = planner.estimate_power(tplan.plan, wl, prof)
+    out["wap_model"] = {
+        "d": tplan.plan.d, "predicted_ms": round(est.t_estimate * 1e3, 4),
+        "predicted_compute_ms": round(est.t_c_total * 1e3, 4), "measured_ms": round(ms, 4),
+        "measured_over_predicted": round(ms / (est.t_estimate * 1e3), 4),
+        "predicted_power_w": round(pw, 1),
+        "predicted_gpu_power_w": round((pw - prof.host_power) / tplan.plan.d, 1),
+        "measured_gpu_power_w": clocks.get("power_w"),
+        "profile": prof.name,
+    }
+    return out, clocks
 
 
 def _count_launches(prog) -> int:
