@@ -94,3 +94,39 @@ def test_plan_training_pipeline():
     assert tp.plan.d == 1  # Table-2 analog: small batch stays on one device
     tp8 = trainer.plan_training(g, 4, planner.load_profile("pcie-box"), force_d=4)
     assert tp8.plan.d == 4 and any(n.kind is ir.OpKind.ALL_REDUCE_SUM for n in tp8.graph)
+
+
+def _ar_worker(rank, world, port, q):
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+    import allreduce_sweep
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, allreduce_sweep.sweep(10_007, 4096, 2, torch.device("cpu"), "gloo")))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allreduce_sweep_harness_gloo():
+    """configs[4] harness (tools/allreduce_sweep.py): single-shot and bucketed SUM
+    allreduce produce the exact sum on every rank; ragged last bucket included."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ar_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, rows in res:
+        assert [r["mode"] for r in rows] == ["single", "bucketed"]
+        assert rows[1]["buckets"] == -(-10_007 // 1024)
+        assert all(r["sum_ok"] for r in rows)
