@@ -934,7 +934,7 @@ __global__ void __launch_bounds__(256) lrn_fast_kernel(const float* __restrict__
 // per lane, the +-2 channel window crosses lanes through 16-wide shuffles.
 // One coalesced read of x (+dy, mask) and one write per element: HBM-bound.
 template <int VPL, bool BWD>
-__global__ void __launch_bounds__(256) lrn_warp_kernel(const float* __restrict__ x, wap_layout_t xl,
+__global__ void __launch_bounds__(256, VPL == 1 ? (BWD ? 6 : 8) : 2) lrn_warp_kernel(const float* __restrict__ x, wap_layout_t xl,
                                                        const float* __restrict__ dy, wap_layout_t dyl, float alpha,
                                                        float beta, float k, float* __restrict__ out, wap_layout_t ol,
                                                        const float* __restrict__ mask, wap_layout_t ml) {
