@@ -173,6 +173,15 @@ int wap_lrn_fwd(const float* x, wap_layout_t xl, int size, float alpha, float be
 int wap_lrn_bwd(const float* x, wap_layout_t xl, const float* dy, wap_layout_t dyl, int size, float alpha,
                 float beta, float bias, float* dx, wap_layout_t dxl, const float* mask, wap_layout_t ml,
                 void* stream);
+/* Fused GradMaxPool -> GradLRN (-> GradReLU) for a stride-2 MaxPool whose input is the
+ * output of an LRN over x (AlexNet norm1 -> pool1, norm2 -> pool2): dx = GradLRN(x,
+ * GradMaxPool(argmax, dy)) * [mask > 0], without materialising the pool gradient.
+ * Same floats as wap_maxpool_bwd followed by wap_lrn_bwd. Replaces the two
+ * interp.py branches for GradMaxPool / GradLRN (extension ops, oracle/interp_ref.py).
+ * Window 2 or 3, LRN size 5, C = 64 or 192, compact channel layouts. */
+int wap_maxpool_lrn_bwd(const uint8_t* argmax, const float* dy, wap_layout_t dyl, int window, int stride,
+                        const float* x, wap_layout_t xl, int size, float alpha, float beta, float bias, float* dx,
+                        wap_layout_t dxl, const float* mask, wap_layout_t ml, void* stream);
 /* Fused SoftmaxXentLoss + GradSoftmaxXent (interp.py:170-175,199-202):
  * loss[0] = sum_rows -(y . logsoftmax(z)) / rows; dz = (softmax(z) - y) / denominator.
  * `work` holds `rows` floats (per-row losses, summed in row order). */

@@ -930,38 +930,16 @@ __global__ void __launch_bounds__(256) lrn_fast_kernel(const float* __restrict__
   }
 }
 
-// Register-only LRN (size 5): 16 lanes per pixel, VPL float4 (4*VPL channels)
-// per lane, the +-2 channel window crosses lanes through 16-wide shuffles.
-// One coalesced read of x (+dy, mask) and one write per element: HBM-bound.
+// LRN (size 5) of one lane's 4*VPL contiguous channels of a pixel whose channels are
+// spread over 16 lanes (lane sl of its half-warp): forward y = x * s^-beta, backward
+// dx = dy * s^-beta - 2*alpha*beta * x * sum_window(dy * x * s^-beta / s), the +-2
+// channel window crossing lanes through 16-wide shuffles. Shared by the LRN kernels
+// and the fused MaxPool+LRN backward, so both produce the same floats.
 template <int VPL, bool BWD>
-__global__ void __launch_bounds__(256, VPL == 1 ? (BWD ? 6 : 8) : 2) lrn_warp_kernel(const float* __restrict__ x, wap_layout_t xl,
-                                                       const float* __restrict__ dy, wap_layout_t dyl, float alpha,
-                                                       float beta, float k, float* __restrict__ out, wap_layout_t ol,
-                                                       const float* __restrict__ mask, wap_layout_t ml) {
+__device__ __forceinline__ void lrn_lane(const float* v, const float* d, int sl, float alpha, float beta, float k,
+                                         float* o) {
   constexpr int NV = 4 * VPL;
-  const int lane = threadIdx.x & 31;
-  const int sl = lane & 15;
-  const bool mask_is_x = BWD && mask == x && ml.pad == xl.pad && ml.ld == xl.ld;
-  const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
-  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int c0 = sl * NV;
-  for (int64_t pbase = wid * 2; pbase < npix; pbase += nw * 2) {
-    const int64_t p = pbase + (lane >> 4);
-    const bool ok = p < npix;
-    int b = 0, h = 0, w = 0;
-    if (ok) pixel_of(xl, p, b, h, w);
-    float v[NV], d[NV], q[NV];
-#pragma unroll
-    for (int i = 0; i < VPL; ++i) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), g = a;
-      if (ok) {
-        a = *reinterpret_cast<const float4*>(x + lidx(xl, b, h, w, c0 + 4 * i));
-        if (BWD) g = *reinterpret_cast<const float4*>(dy + lidx(dyl, b, h, w, c0 + 4 * i));
-      }
-      v[4 * i] = a.x; v[4 * i + 1] = a.y; v[4 * i + 2] = a.z; v[4 * i + 3] = a.w;
-      d[4 * i] = g.x; d[4 * i + 1] = g.y; d[4 * i + 2] = g.z; d[4 * i + 3] = g.w;
-    }
+  float q[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) q[j] = v[j] * v[j];
     // window sums of squares over channels c-2..c+2
@@ -980,7 +958,6 @@ __global__ void __launch_bounds__(256, VPL == 1 ? (BWD ? 6 : 8) : 2) lrn_warp_ke
       s[j] = k + alpha * acc;
       pw[j] = exp2f(-beta * __log2f(s[j]));
     }
-    float o[NV];
     if (!BWD) {
 #pragma unroll
       for (int j = 0; j < NV; ++j) o[j] = v[j] * pw[j];
@@ -1002,6 +979,42 @@ __global__ void __launch_bounds__(256, VPL == 1 ? (BWD ? 6 : 8) : 2) lrn_warp_ke
         o[j] = d[j] * pw[j] - 2.f * alpha * beta * v[j] * acc;
       }
     }
+}
+
+// Register-only LRN (size 5): 16 lanes per pixel, VPL float4 (4*VPL channels)
+// per lane, the +-2 channel window crosses lanes through 16-wide shuffles.
+// One coalesced read of x (+dy, mask) and one write per element: HBM-bound.
+template <int VPL, bool BWD>
+__global__ void __launch_bounds__(256, VPL == 1 ? (BWD ? 6 : 8) : 2) lrn_warp_kernel(const float* __restrict__ x, wap_layout_t xl,
+                                                       const float* __restrict__ dy, wap_layout_t dyl, float alpha,
+                                                       float beta, float k, float* __restrict__ out, wap_layout_t ol,
+                                                       const float* __restrict__ mask, wap_layout_t ml) {
+  constexpr int NV = 4 * VPL;
+  const int lane = threadIdx.x & 31;
+  const int sl = lane & 15;
+  const bool mask_is_x = BWD && mask == x && ml.pad == xl.pad && ml.ld == xl.ld;
+  const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int c0 = sl * NV;
+  for (int64_t pbase = wid * 2; pbase < npix; pbase += nw * 2) {
+    const int64_t p = pbase + (lane >> 4);
+    const bool ok = p < npix;
+    int b = 0, h = 0, w = 0;
+    if (ok) pixel_of(xl, p, b, h, w);
+    float v[NV], d[NV];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), g = a;
+      if (ok) {
+        a = *reinterpret_cast<const float4*>(x + lidx(xl, b, h, w, c0 + 4 * i));
+        if (BWD) g = *reinterpret_cast<const float4*>(dy + lidx(dyl, b, h, w, c0 + 4 * i));
+      }
+      v[4 * i] = a.x; v[4 * i + 1] = a.y; v[4 * i + 2] = a.z; v[4 * i + 3] = a.w;
+      d[4 * i] = g.x; d[4 * i + 1] = g.y; d[4 * i + 2] = g.z; d[4 * i + 3] = g.w;
+    }
+    float o[NV];
+    lrn_lane<VPL, BWD>(v, d, sl, alpha, beta, k, o);
     if (!ok) continue;
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
@@ -1020,6 +1033,112 @@ __global__ void __launch_bounds__(256, VPL == 1 ? (BWD ? 6 : 8) : 2) lrn_warp_ke
         if (!(m.w > 0.f)) r.w = 0.f;
       }
       *reinterpret_cast<float4*>(out + lidx(ol, b, h, w, c0 + 4 * i)) = r;
+    }
+  }
+}
+
+// Fused MaxPool backward (stride 2) -> LRN backward (size 5) -> GradReLU, for a
+// MaxPool whose input is an LRN output (AlexNet norm1 -> pool1, norm2 -> pool2):
+// a half-warp owns one 2x2 block of pooled-from pixels, lane sl the 4*VPL contiguous
+// channels lrn_lane expects. The pool gradient of the block is gathered exactly as
+// maxpool_bwd_s2_kernel does (same window order) and stays in registers as the LRN's
+// dy, so the intermediate tensor is never written or re-read.
+template <int WIN, int VPL>
+__global__ void __launch_bounds__(256, VPL == 1 ? 4 : 2) maxpool_lrn_bwd_kernel(
+    const uint8_t* __restrict__ arg, const float* __restrict__ dy, wap_layout_t yl, const float* __restrict__ x,
+    wap_layout_t xl, float alpha, float beta, float k, float* __restrict__ out, wap_layout_t ol,
+    const float* __restrict__ mask, wap_layout_t ml) {
+  constexpr int NW = WIN - 1;
+  constexpr int NV = 4 * VPL;
+  const int lane = threadIdx.x & 31;
+  const int sl = lane & 15;
+  const int c0 = sl * NV;
+  const bool mask_is_x = mask == x && ml.pad == xl.pad && ml.ld == xl.ld;
+  const uint32_t PH = (xl.H + 1) >> 1, PW = (xl.W + 1) >> 1;
+  const int64_t nblk = (int64_t)xl.B * PH * PW;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t pbase = wid * 2; pbase < nblk; pbase += nw * 2) {  // warp-uniform trip count
+    const int64_t blk = pbase + (lane >> 4);
+    const bool ok = blk < nblk;
+    int b = 0, i = 0, jj = 0;
+    if (ok) {
+      const uint32_t q = (uint32_t)blk, r = q / PW;
+      jj = (int)(q - r * PW);
+      b = (int)(r / PH);
+      i = (int)(r - (uint32_t)b * PH);
+    }
+    float g[2][2][NV];
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) g[p][qq][j] = 0.f;
+#pragma unroll
+    for (int a = 0; a < NW; ++a) {
+      const int ho = i - (NW - 1) + a;
+#pragma unroll
+      for (int bb = 0; bb < NW; ++bb) {
+        const int wo = jj - (NW - 1) + bb;
+        if (!ok || ho < 0 || ho >= yl.H || wo < 0 || wo >= yl.W) continue;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          const int64_t yi = lidx(yl, b, ho, wo, c0 + 4 * v);
+          const uchar4 a4 = *reinterpret_cast<const uchar4*>(arg + yi);
+          const float4 gv = __ldg(reinterpret_cast<const float4*>(dy + yi));
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            const int r = 2 * (NW - 1 - a) + p;
+            if (r >= WIN) continue;
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq) {
+              const int cc = 2 * (NW - 1 - bb) + qq;
+              if (cc >= WIN) continue;
+              const int local = r * WIN + cc;
+              float* gg = &g[p][qq][4 * v];
+              if (a4.x == local) gg[0] += gv.x;
+              if (a4.y == local) gg[1] += gv.y;
+              if (a4.z == local) gg[2] += gv.z;
+              if (a4.w == local) gg[3] += gv.w;
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq) {
+        const int h = 2 * i + p, w = 2 * jj + qq;
+        const bool pix = ok && h < xl.H && w < xl.W;
+        float v[NV], o[NV];
+#pragma unroll
+        for (int t = 0; t < VPL; ++t) {
+          float4 xa = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (pix) xa = *reinterpret_cast<const float4*>(x + lidx(xl, b, h, w, c0 + 4 * t));
+          v[4 * t] = xa.x; v[4 * t + 1] = xa.y; v[4 * t + 2] = xa.z; v[4 * t + 3] = xa.w;
+        }
+        lrn_lane<VPL, true>(v, g[p][qq], sl, alpha, beta, k, o);  // every lane: shuffles
+        if (!pix) continue;
+#pragma unroll
+        for (int t = 0; t < VPL; ++t) {
+          float4 rr = make_float4(o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
+          if (mask_is_x) {
+            if (!(v[4 * t] > 0.f)) rr.x = 0.f;
+            if (!(v[4 * t + 1] > 0.f)) rr.y = 0.f;
+            if (!(v[4 * t + 2] > 0.f)) rr.z = 0.f;
+            if (!(v[4 * t + 3] > 0.f)) rr.w = 0.f;
+          } else if (mask) {
+            const float4 m = *reinterpret_cast<const float4*>(mask + lidx(ml, b, h, w, c0 + 4 * t));
+            if (!(m.x > 0.f)) rr.x = 0.f;
+            if (!(m.y > 0.f)) rr.y = 0.f;
+            if (!(m.z > 0.f)) rr.z = 0.f;
+            if (!(m.w > 0.f)) rr.w = 0.f;
+          }
+          *reinterpret_cast<float4*>(out + lidx(ol, b, h, w, c0 + 4 * t)) = rr;
+        }
+      }
     }
   }
 }
@@ -1382,6 +1501,41 @@ extern "C" int wap_maxpool_bwd(const uint8_t* argmax, const float* dy, wap_layou
     maxpool_bwd_kernel<2, 2><<<grid, 256, 0, STREAM(stream)>>>(argmax, dy, dyl, window, stride, dx, dxl, mask, ml);
   else
     maxpool_bwd_kernel<0, 0><<<grid, 256, 0, STREAM(stream)>>>(argmax, dy, dyl, window, stride, dx, dxl, mask, ml);
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
+  return WAP_OK;
+}
+
+extern "C" int wap_maxpool_lrn_bwd(const uint8_t* argmax, const float* dy, wap_layout_t dyl, int window,
+                                   int stride, const float* x, wap_layout_t xl, int size, float alpha, float beta,
+                                   float bias, float* dx, wap_layout_t dxl, const float* mask, wap_layout_t ml,
+                                   void* stream) {
+  int rc;
+  if ((rc = check_layout(dyl, "dy")) || (rc = check_layout(xl, "x")) || (rc = check_layout(dxl, "dx"))) return rc;
+  if (mask && (rc = check_layout(ml, "mask"))) return rc;
+  WAP_CHECK_ARG(argmax != nullptr, "maxpool backward needs the forward argmax");
+  WAP_CHECK_ARG(stride == 2 && (window == 2 || window == 3) && size == 5,
+                "fused maxpool+lrn backward: stride 2, window 2/3, LRN size 5 only");
+  WAP_CHECK_ARG(xl.C == 64 || xl.C == 192, "fused maxpool+lrn backward: C must be 64 or 192");
+  WAP_CHECK_ARG(xl.ld == xl.C && dxl.ld == xl.C && dyl.ld == xl.C && (!mask || ml.ld == xl.C),
+                "fused maxpool+lrn backward: compact channel layouts only");
+  WAP_CHECK_ARG(dyl.H == (xl.H - window) / 2 + 1 && dyl.W == (xl.W - window) / 2 + 1 && dyl.B == xl.B &&
+                    dxl.H == xl.H && dxl.W == xl.W && dxl.B == xl.B && dxl.C == xl.C,
+                "fused maxpool+lrn backward: layouts do not match");
+  const int64_t nblk = (int64_t)xl.B * ((xl.H + 1) / 2) * ((xl.W + 1) / 2);
+  WAP_CHECK_ARG(nblk < (1LL << 31), "fused maxpool+lrn backward: too many pixels");
+  int64_t blocks = ((nblk + 1) / 2 * 32 + 255) / 256;
+  if (blocks > (int64_t)WAP_NUM_SMS * 16) blocks = (int64_t)WAP_NUM_SMS * 16;
+  cudaStream_t st = STREAM(stream);
+#define WAP_MPLRN(WIN, VPL)                                                                                    \
+  maxpool_lrn_bwd_kernel<WIN, VPL><<<(int)blocks, 256, 0, st>>>(argmax, dy, dyl, x, xl, alpha, beta, bias, dx, \
+                                                                  dxl, mask, ml)
+  if (window == 3) {
+    if (xl.C == 64) WAP_MPLRN(3, 1); else WAP_MPLRN(3, 3);
+  } else {
+    if (xl.C == 64) WAP_MPLRN(2, 1); else WAP_MPLRN(2, 3);
+  }
+#undef WAP_MPLRN
   WAP_LAUNCH_CHECK();
   COUNT_LAUNCH();
   return WAP_OK;

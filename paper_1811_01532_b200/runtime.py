@@ -287,6 +287,7 @@ class Program:
                 self.xent.setdefault(key, {})["loss" if n.kind is OpKind.SOFTMAX_XENT_LOSS else "grad"] = nid
         # MaxPool argmax owners: (input, window, stride) -> MaxPool node
         self.pool_of: dict[tuple, str] = {}
+        self._pool_lrn: dict[str, tuple] = {}  # GradLRN id -> its fused GradMaxPool operands
         for nid in self.order:
             n = self.node(nid)
             if n.kind is OpKind.MAX_POOL:
@@ -1126,6 +1127,11 @@ class Program:
         arg = self.t[f"{pool}::argmax"]
         dy = self._in(n, dy_id)
         gr = self.bwd_mask.get(n.id)
+        lrn = self._pool_lrn_fusable(n, gr, dy)
+        if lrn is not None:
+            # GradMaxPool -> GradLRN as one kernel (wap_maxpool_lrn_bwd), emitted at the GradLRN
+            self._pool_lrn[lrn] = (arg, dy, n.attr("window"), n.attr("stride"))
+            return
         out = self._out(gr if gr else n.id)
         mask = self._in(self.node(gr), self.mask_src(self.node(gr).inputs[0])) if gr else None
         if pool in self.pool_relu_fused:
@@ -1146,14 +1152,45 @@ class Program:
                    (x.ptr, x.layout(), a["size"], C.c_float(a["alpha"]), C.c_float(a["beta"]), C.c_float(a["bias"]),
                     y.ptr, y.layout()), "LRN", alg_bytes=self._nbytes(x, y))
 
+    def _pool_lrn_fusable(self, n: Node, gr, dy) -> str | None:
+        """The GradLRN consuming this GradMaxPool's output when the pair can run fused:
+        sole consumer, not a graph output, no GradReLU on the pool gradient, stride 2,
+        window 2/3, LRN size 5 over C = 64 / 192 compact channels."""
+        if os.environ.get("WAP_FUSE_POOL_LRN", "1") == "0" or gr or n.id in self.g.outputs:
+            return None
+        users = self.users.get(n.id, [])
+        if len(users) != 1 or self.kind(users[0]) is not OpKind.GRAD_LRN:
+            return None
+        ln = self.node(users[0])
+        if ln.inputs[1] != n.id or ln.inputs[0] == n.id or ln.attr("size") != 5:
+            return None
+        if n.attr("stride") != 2 or n.attr("window") not in (2, 3):
+            return None
+        x = self.t.get(ln.inputs[0])
+        if x is None or x.kind != "nhwc" or x.dims[-1] not in (64, 192) or x.ld != x.dims[-1] or dy.ld != x.ld:
+            return None
+        return ln.id
+
     def _lower_lrn_grad(self, n: Node) -> None:
         x = self._in(n, n.inputs[0])
-        dy = self._in(n, n.inputs[1])
         gr = self.bwd_mask.get(n.id)
         out = self._out(gr if gr else n.id)
         mask = self._in(self.node(gr), self.mask_src(self.node(gr).inputs[0])) if gr else None
         ml = mask.layout() if mask is not None else N.wap_layout_t()
         a = n.attrs
+        fused = self._pool_lrn.pop(n.id, None)
+        if fused is not None and out.ld == x.ld and (mask is None or mask.ld == x.ld):
+            arg, pdy, window, stride = fused
+            self._emit(n.id, self.L.wap_maxpool_lrn_bwd,
+                       (arg.ptr, pdy.ptr, pdy.layout(), window, stride, x.ptr, x.layout(), a["size"],
+                        C.c_float(a["alpha"]), C.c_float(a["beta"]), C.c_float(a["bias"]), out.ptr, out.layout(),
+                        mask.ptr if mask is not None else None, ml), "GradMaxPool+GradLRN",
+                       alg_bytes=self._nbytes(pdy, x, out) + self._nbytes(pdy) // 4
+                       + (0 if mask is None or mask.ptr == x.ptr else self._nbytes(mask)))
+            return
+        if fused is not None:
+            raise EvalError(f"{n.id!r}: fused MaxPool+LRN backward needs compact channel layouts")
+        dy = self._in(n, n.inputs[1])
         self._emit(n.id, self.L.wap_lrn_bwd,
                    (x.ptr, x.layout(), dy.ptr, dy.layout(), a["size"], C.c_float(a["alpha"]), C.c_float(a["beta"]),
                     C.c_float(a["bias"]), out.ptr, out.layout(), mask.ptr if mask is not None else None, ml),

@@ -88,3 +88,45 @@ def test_pack_images_c3(cuda, B, H, W, pad):
     assert (dst[:, :H, :W, 3] == 0).all()
     if pad:
         assert torch.isnan(dst[:, H:, :, :3]).all() and torch.isnan(dst[:, :, W:, :3]).all()
+
+
+@pytest.mark.parametrize("B,H,C,win,pad,relu_mask", [
+    (2, 55, 64, 3, 2, True),    # AlexNet conv1 -> ReLU -> norm1 -> pool1 (mask = LRN input)
+    (2, 27, 192, 3, 0, True),   # conv2 -> ReLU -> norm2 -> pool2
+    (1, 13, 64, 3, 1, False),   # no GradReLU
+    (2, 16, 192, 2, 0, False),  # window 2
+])
+def test_maxpool_lrn_bwd_fused_matches_unfused(cuda, B, H, C, win, pad, relu_mask):
+    """wap_maxpool_lrn_bwd == wap_maxpool_bwd followed by wap_lrn_bwd (same floats)."""
+    L = N.lib()
+    W, s = H, 2
+    Ho = (H - win) // s + 1
+    a, beta, k = 1e-4, 0.75, 2.0
+    g = torch.Generator(device="cuda").manual_seed(21)
+    x = torch.zeros(B, H + pad, W + pad, C, device=cuda)
+    x[:, :H, :W] = torch.randn(B, H, W, C, device=cuda, generator=g) * 3
+    xl = N.wap_layout_t(B, H, W, C, pad, C)
+    y = torch.zeros_like(x)
+    N.check(L.wap_lrn_fwd(x.data_ptr(), xl, 5, a, beta, k, y.data_ptr(), xl, None))
+    yl = N.wap_layout_t(B, Ho, Ho, C, 0, C)
+    yp = torch.zeros(B, Ho, Ho, C, device=cuda)
+    arg = torch.zeros(B * Ho * Ho * C, dtype=torch.uint8, device=cuda)
+    N.check(L.wap_maxpool_fwd_ex(y.data_ptr(), xl, win, s, yp.data_ptr(), yl, arg.data_ptr(), 0, None))
+    dy = torch.randn(B, Ho, Ho, C, device=cuda, generator=g)
+    mask = x if relu_mask else None
+    mptr = mask.data_ptr() if mask is not None else None
+    # unfused: pool gradient tensor, then LRN backward
+    dpool = torch.zeros_like(x)
+    N.check(L.wap_maxpool_bwd(arg.data_ptr(), dy.data_ptr(), yl, win, s, dpool.data_ptr(), xl, None, xl, None))
+    ref = torch.full_like(x, float("nan"))
+    N.check(L.wap_lrn_bwd(x.data_ptr(), xl, dpool.data_ptr(), xl, 5, a, beta, k, ref.data_ptr(), xl, mptr, xl,
+                          None))
+    got = torch.full_like(x, float("nan"))
+    N.check(L.wap_maxpool_lrn_bwd(arg.data_ptr(), dy.data_ptr(), yl, win, s, x.data_ptr(), xl, 5, a, beta, k,
+                                  got.data_ptr(), xl, mptr, xl, None))
+    torch.cuda.synchronize()
+    r, o = ref[:, :H, :W], got[:, :H, :W]
+    assert not torch.isnan(o).any()
+    assert ((r - o).abs().max() / r.abs().max()).item() < 1e-6
+    if pad:
+        assert torch.isnan(got[:, H:]).all() and torch.isnan(got[:, :, W:]).all()
