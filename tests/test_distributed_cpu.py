@@ -51,7 +51,8 @@ def _worker(rank, world, port, model, batch, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("model,batch,world", [("alexnet_like", 16, 2), ("mlp", 24, 4), ("vgg16_like", 8, 2)])
+@pytest.mark.parametrize("model,batch,world", [("alexnet_like", 16, 2), ("mlp", 24, 4), ("vgg16_like", 8, 2),
+                                               ("alexnet_like", 12, 3), ("mlp", 30, 5)])
 def test_rank_views_with_gloo_allreduce(model, batch, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
