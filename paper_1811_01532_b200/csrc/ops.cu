@@ -1037,6 +1037,46 @@ __global__ void __launch_bounds__(256, VPL == 1 ? (BWD ? 6 : 8) : 2) lrn_warp_ke
   }
 }
 
+// LRN forward, C = 64: lrn_warp_kernel<1, false> with U pixel pairs per warp
+// iteration whose loads are all issued before any math (2x the bytes in flight of
+// the one-pair loop). Same lrn_lane math, same floats.
+template <int U>
+__global__ void __launch_bounds__(256, 8) lrn_fwd_c64_kernel(const float* __restrict__ x, wap_layout_t xl,
+                                                             float alpha, float beta, float k,
+                                                             float* __restrict__ out, wap_layout_t ol) {
+  const int lane = threadIdx.x & 31;
+  const int sl = lane & 15;
+  const int64_t npix = (int64_t)xl.B * xl.H * xl.W;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int c0 = sl * 4;
+  for (int64_t pbase = wid * 2 * U; pbase < npix; pbase += nw * 2 * U) {
+    float v[U][4];
+    int64_t oi[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = pbase + 2 * u + (lane >> 4);
+      ok[u] = p < npix;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      oi[u] = 0;
+      if (ok[u]) {
+        int b, h, w;
+        pixel_of(xl, p, b, h, w);
+        a = *reinterpret_cast<const float4*>(x + lidx(xl, b, h, w, c0));
+        oi[u] = lidx(ol, b, h, w, c0);
+      }
+      v[u][0] = a.x; v[u][1] = a.y; v[u][2] = a.z; v[u][3] = a.w;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float o[4];
+      lrn_lane<1, false>(v[u], v[u], sl, alpha, beta, k, o);
+      if (ok[u]) *reinterpret_cast<float4*>(out + oi[u]) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
 // Fused MaxPool backward (stride 2) -> LRN backward (size 5) -> GradReLU, for a
 // MaxPool whose input is an LRN output (AlexNet norm1 -> pool1, norm2 -> pool2):
 // a half-warp owns one 2x2 block of pooled-from pixels, lane sl the 4*VPL contiguous
@@ -1154,7 +1194,12 @@ bool launch_lrn_fast(const float* x, wap_layout_t xl, const float* dy, wap_layou
     const int64_t warps = (npix + 1) / 2;
     int64_t blocks = (warps * 32 + 255) / 256;
     if (blocks > (int64_t)WAP_NUM_SMS * 16) blocks = (int64_t)WAP_NUM_SMS * 16;
-    if (xl.C == 64)
+    if (xl.C == 64 && !BWD) {
+      const int64_t w2 = (npix + 3) / 4;  // two pixel pairs per warp iteration
+      int64_t b2 = (w2 * 32 + 255) / 256;
+      if (b2 > (int64_t)WAP_NUM_SMS * 8) b2 = (int64_t)WAP_NUM_SMS * 8;
+      lrn_fwd_c64_kernel<2><<<(int)b2, 256, 0, st>>>(x, xl, alpha, beta, bias, out, ol);
+    } else if (xl.C == 64)
       lrn_warp_kernel<1, BWD><<<(int)blocks, 256, 0, st>>>(x, xl, dy, dyl, alpha, beta, bias, out, ol, mask, ml);
     else
       lrn_warp_kernel<3, BWD><<<(int)blocks, 256, 0, st>>>(x, xl, dy, dyl, alpha, beta, bias, out, ol, mask, ml);

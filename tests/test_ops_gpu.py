@@ -130,3 +130,28 @@ def test_maxpool_lrn_bwd_fused_matches_unfused(cuda, B, H, C, win, pad, relu_mas
     assert ((r - o).abs().max() / r.abs().max()).item() < 1e-6
     if pad:
         assert torch.isnan(got[:, H:]).all() and torch.isnan(got[:, :, W:]).all()
+
+
+def _lrn_ref(x, size, alpha, beta, k):
+    """LRN across channels, NHWC fp64 (oracle/interp_ref.py rule)."""
+    x = x.double()
+    sq = F.pad(x * x, (size // 2, size // 2))
+    s = sum(sq[..., i:i + x.shape[-1]] for i in range(size))
+    return x * (k + alpha * s) ** (-beta)
+
+
+@pytest.mark.parametrize("B,H,C,pad", [(2, 55, 64, 2), (3, 27, 192, 0), (1, 7, 64, 0)])
+def test_lrn_fwd_vs_torch(cuda, B, H, C, pad):
+    L = N.lib()
+    a, beta, k = 1e-4, 0.75, 2.0
+    g = torch.Generator(device="cuda").manual_seed(31)
+    x = torch.zeros(B, H + pad, H + pad, C, device=cuda)
+    x[:, :H, :H] = torch.randn(B, H, H, C, device=cuda, generator=g) * 4
+    xl = N.wap_layout_t(B, H, H, C, pad, C)
+    y = torch.full_like(x, float("nan"))
+    N.check(L.wap_lrn_fwd(x.data_ptr(), xl, 5, a, beta, k, y.data_ptr(), xl, None))
+    torch.cuda.synchronize()
+    ref = _lrn_ref(x[:, :H, :H], 5, a, beta, k)
+    assert ((y[:, :H, :H].double() - ref).abs().max() / ref.abs().max()).item() < 2e-6
+    if pad:
+        assert torch.isnan(y[:, H:]).all()
