@@ -540,6 +540,89 @@ __global__ void __launch_bounds__(256) conv_direct_kernel(const float* __restric
   }
 }
 
+// conv_direct_kernel<3, 3> with two horizontally adjacent output pixels per thread:
+// every broadcast weight load feeds two FMAs (the one-pixel kernel issues one LDS.128
+// per 4 FMAs and is shared-memory-issue bound), and the two pixels share 2 of their 3
+// input columns (12 loads instead of 18). Per-pixel FMA order is unchanged, so the
+// outputs are the same floats as the one-pixel kernel.
+__global__ void __launch_bounds__(256, 2) conv_direct_3x3c3_px2_kernel(const float* __restrict__ x, wap_layout_t xl,
+                                                                    const float* __restrict__ w, int p, int ldw,
+                                                                    const float* __restrict__ bias, int relu,
+                                                                    float* __restrict__ y, wap_layout_t yl,
+                                                                    uint32_t* __restrict__ mbits, int64_t mbits_ld) {
+  constexpr int C = 3, K = 27;
+  extern __shared__ __align__(16) float ws[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = blockIdx.y;
+  for (int i = threadIdx.x; i < K * 32; i += blockDim.x) ws[i] = w[(int64_t)(i >> 5) * ldw + grp * 32 + (i & 31)];
+  if (threadIdx.x < 32) ws[K * 32 + threadIdx.x] = bias ? bias[grp * 32 + threadIdx.x] : 0.f;
+  __syncthreads();
+  const float4* ws4 = reinterpret_cast<const float4*>(ws);
+  const uint32_t Wp = ((uint32_t)yl.W + 1) >> 1;
+  const uint32_t npair = (uint32_t)yl.B * yl.H * Wp;
+  for (uint32_t pp = (blockIdx.x * 8 + warp) * 32 + lane; pp < npair; pp += gridDim.x * 256) {
+    const uint32_t jq = pp % Wp, r = pp / Wp;
+    const int h = (int)(r % (uint32_t)yl.H), bb = (int)(r / (uint32_t)yl.H), wo = (int)jq * 2;
+    const bool two = wo + 1 < yl.W;
+    float acc[2][32];
+#pragma unroll
+    for (int o4 = 0; o4 < 8; ++o4) {
+      const float4 bq = ws4[K * 8 + o4];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        acc[e][4 * o4] = bq.x; acc[e][4 * o4 + 1] = bq.y; acc[e][4 * o4 + 2] = bq.z; acc[e][4 * o4 + 3] = bq.w;
+      }
+    }
+#pragma unroll 1
+    for (int u = 0; u < 3; ++u) {
+      const int hi = h + u - p;
+      float xa[4][4];  // input columns wo-p .. wo-p+3
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int wi = wo + cc - p;
+        float4 xv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (hi >= 0 && hi < xl.H && wi >= 0 && wi < xl.W)
+          xv = __ldg(reinterpret_cast<const float4*>(x + lidx(xl, bb, hi, wi, 0)));
+        xa[cc][0] = xv.x; xa[cc][1] = xv.y; xa[cc][2] = xv.z; xa[cc][3] = xv.w;
+      }
+#pragma unroll
+      for (int v = 0; v < 3; ++v) {
+        const float4* wt = ws4 + (u * 3 + v) * C * 8;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+#pragma unroll
+          for (int o4 = 0; o4 < 8; ++o4) {
+            const float4 wq4 = wt[c * 8 + o4];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const float xe = xa[v + e][c];
+              acc[e][4 * o4] = fmaf(xe, wq4.x, acc[e][4 * o4]);
+              acc[e][4 * o4 + 1] = fmaf(xe, wq4.y, acc[e][4 * o4 + 1]);
+              acc[e][4 * o4 + 2] = fmaf(xe, wq4.z, acc[e][4 * o4 + 2]);
+              acc[e][4 * o4 + 3] = fmaf(xe, wq4.w, acc[e][4 * o4 + 3]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      if (e == 1 && !two) break;
+      const int64_t yrow = ((int64_t)bb * (yl.H + yl.pad) + h) * (yl.W + yl.pad) + wo + e;
+      float* dst = y + yrow * yl.ld + grp * 32;
+      uint32_t bits = 0;
+#pragma unroll
+      for (int o = 0; o < 32; o += 4) {
+        float4 q = make_float4(acc[e][o], acc[e][o + 1], acc[e][o + 2], acc[e][o + 3]);
+        if (relu) q = make_float4(fmaxf(q.x, 0.f), fmaxf(q.y, 0.f), fmaxf(q.z, 0.f), fmaxf(q.w, 0.f));
+        bits |= ((q.x > 0.f) << o) | ((q.y > 0.f) << (o + 1)) | ((q.z > 0.f) << (o + 2)) | ((q.w > 0.f) << (o + 3));
+        *reinterpret_cast<float4*>(dst + o) = q;
+      }
+      if (mbits) mbits[yrow * mbits_ld + grp] = bits;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // MaxPool
 // ---------------------------------------------------------------------------
@@ -1413,7 +1496,12 @@ extern "C" int wap_conv_direct(const float* x, wap_layout_t xl, const float* w, 
   int64_t bx = (npix + 255) / 256;
   if (bx > (int64_t)WAP_NUM_SMS * 16) bx = (int64_t)WAP_NUM_SMS * 16;
   const dim3 grid((unsigned)bx, (unsigned)(yl.C / 32));
-  if (k == 3 && xl.C == 3)
+  if (k == 3 && xl.C == 3 && !getenv("WAP_CONV_DIRECT_PX1")) {
+    int64_t b2 = ((int64_t)yl.B * yl.H * ((yl.W + 1) / 2) + 255) / 256;
+    if (b2 > (int64_t)WAP_NUM_SMS * 16) b2 = (int64_t)WAP_NUM_SMS * 16;
+    conv_direct_3x3c3_px2_kernel<<<dim3((unsigned)b2, (unsigned)(yl.C / 32)), 256, smem, STREAM(stream)>>>(
+        x, xl, w, padding, ldw, bias, relu, y, yl, mbits, mbits_ld);
+  } else if (k == 3 && xl.C == 3)
     conv_direct_kernel<3, 3><<<grid, 256, smem, STREAM(stream)>>>(x, xl, w, k, padding, ldw, bias, relu, y, yl, mbits,
                                                                 mbits_ld);
   else

@@ -155,3 +155,39 @@ def test_lrn_fwd_vs_torch(cuda, B, H, C, pad):
     assert ((y[:, :H, :H].double() - ref).abs().max() / ref.abs().max()).item() < 2e-6
     if pad:
         assert torch.isnan(y[:, H:]).all()
+
+
+@pytest.mark.parametrize("B,H,W,pad", [(2, 224, 224, 1), (1, 9, 7, 1), (2, 5, 6, 0)])
+def test_conv_direct_3x3_c3(cuda, B, H, W, pad):
+    """VGG-16 conv1_1 direct conv (wap_conv_direct, 3x3 same, C=3): the two-pixel kernel
+    equals the one-pixel kernel bit for bit (outputs and ReLU mask bits) and torch fp64."""
+    L = N.lib()
+    Co = 64
+    g = torch.Generator(device="cuda").manual_seed(41)
+    x = torch.zeros(B, H, W, 4, device=cuda)
+    x[..., :3] = torch.randn(B, H, W, 3, device=cuda, generator=g)
+    w = torch.randn(27, Co, device=cuda, generator=g) * 0.2
+    bias = torch.randn(Co, device=cuda, generator=g) * 0.1
+    xl = N.wap_layout_t(B, H, W, 3, 0, 4)
+    yl = N.wap_layout_t(B, H, W, Co, pad, Co)
+    rows = B * (H + pad) * (W + pad)
+    outs = []
+    for px1 in (False, True):
+        if px1:
+            os.environ["WAP_CONV_DIRECT_PX1"] = "1"
+        try:
+            y = torch.full((B, H + pad, W + pad, Co), float("nan"), device=cuda)
+            bits = torch.zeros(rows, Co // 32, dtype=torch.int32, device=cuda)
+            N.check(L.wap_conv_direct(x.data_ptr(), xl, w.data_ptr(), 3, 1, Co, bias.data_ptr(), 1, y.data_ptr(),
+                                      yl, bits.data_ptr(), Co // 32, None))
+            torch.cuda.synchronize()
+        finally:
+            os.environ.pop("WAP_CONV_DIRECT_PX1", None)
+        outs.append((y, bits))
+    (y2, b2), (y1, b1) = outs
+    assert torch.equal(y2[:, :H, :W], y1[:, :H, :W]) and torch.equal(b2, b1)
+    ref = F.conv2d(x[..., :3].double().permute(0, 3, 1, 2), w.double().view(3, 3, 3, Co).permute(3, 2, 0, 1),
+                   bias.double(), padding=1).relu().permute(0, 2, 3, 1)
+    assert ((y2[:, :H, :W].double() - ref).abs().max() / ref.abs().max()).item() < 1e-6
+    if pad:
+        assert torch.isnan(y2[:, H:]).all() and torch.isnan(y2[:, :, W:]).all()
