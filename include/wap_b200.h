@@ -173,6 +173,12 @@ int wap_lrn_fwd(const float* x, wap_layout_t xl, int size, float alpha, float be
 int wap_lrn_bwd(const float* x, wap_layout_t xl, const float* dy, wap_layout_t dyl, int size, float alpha,
                 float beta, float bias, float* dx, wap_layout_t dxl, const float* mask, wap_layout_t ml,
                 void* stream);
+/* Fused LRN -> MaxPool forward (the LRN output is read by nothing else): y/argmax =
+ * MaxPool(LRN(x)) exactly as wap_lrn_fwd followed by wap_maxpool_fwd (same floats and
+ * argmax), without writing the LRN output. LRN size 5, window 2 or 3, C = 64 or 192,
+ * compact channel layouts. */
+int wap_lrn_maxpool_fwd(const float* x, wap_layout_t xl, int size, float alpha, float beta, float bias, int window,
+                        int stride, float* y, wap_layout_t yl, uint8_t* argmax, void* stream);
 /* Fused GradMaxPool -> GradLRN (-> GradReLU) for a stride-2 MaxPool whose input is the
  * output of an LRN over x (AlexNet norm1 -> pool1, norm2 -> pool2): dx = GradLRN(x,
  * GradMaxPool(argmax, dy)) * [mask > 0], without materialising the pool gradient.

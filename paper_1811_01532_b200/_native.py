@@ -140,6 +140,7 @@ _SIGNATURES: list[tuple[str, object, list]] = [
     ("wap_maxpool_fwd", _I, [_P, wap_layout_t, _I, _I, _P, wap_layout_t, _P, _P]),
     ("wap_maxpool_fwd_ex", _I, [_P, wap_layout_t, _I, _I, _P, wap_layout_t, _P, _I, _P]),
     ("wap_maxpool_bwd", _I, [_P, _P, wap_layout_t, _I, _I, _P, wap_layout_t, _P, wap_layout_t, _P]),
+    ("wap_lrn_maxpool_fwd", _I, [_P, wap_layout_t, _I, _F, _F, _F, _I, _I, _P, wap_layout_t, _P, _P]),
     ("wap_maxpool_lrn_bwd", _I, [_P, _P, wap_layout_t, _I, _I, _P, wap_layout_t, _I, _F, _F, _F, _P,
                                  wap_layout_t, _P, wap_layout_t, _P]),
     ("wap_lrn_fwd", _I, [_P, wap_layout_t, _I, _F, _F, _F, _P, wap_layout_t, _P]),

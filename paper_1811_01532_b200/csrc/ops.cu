@@ -1160,6 +1160,62 @@ __global__ void __launch_bounds__(256, 8) lrn_fwd_c64_kernel(const float* __rest
   }
 }
 
+// Fused LRN (size 5) -> MaxPool forward (AlexNet norm1 -> pool1, norm2 -> pool2) when
+// the LRN output has no other reader: a half-warp owns one pooled pixel, lane sl the
+// 4*VPL channels lrn_lane expects; each window pixel's LRN is computed in registers
+// and max-reduced in maxpool_fwd_kernel's order (rows, then columns; first max wins),
+// so pooled values and argmax are the same as the two-kernel path, and the LRN output
+// tensor is never written or re-read. (Overlapping 3/2 windows recompute 2.25x LRN.)
+template <int WIN, int VPL>
+__global__ void __launch_bounds__(256) lrn_maxpool_fwd_kernel(const float* __restrict__ x, wap_layout_t xl,
+                                                              float alpha, float beta, float k, int s,
+                                                              float* __restrict__ y, wap_layout_t yl,
+                                                              uint8_t* __restrict__ arg) {
+  constexpr int NV = 4 * VPL;
+  const int lane = threadIdx.x & 31;
+  const int sl = lane & 15;
+  const int c0 = sl * NV;
+  const int64_t nout = (int64_t)yl.B * yl.H * yl.W;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t pbase = wid * 2; pbase < nout; pbase += nw * 2) {
+    const int64_t p = pbase + (lane >> 4);
+    const bool ok = p < nout;
+    int b = 0, ho = 0, wo = 0;
+    if (ok) pixel_of(yl, p, b, ho, wo);
+    float best[NV];
+    int bi[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) { best[j] = -INFINITY; bi[j] = 0; }
+#pragma unroll
+    for (int a2 = 0; a2 < WIN; ++a2) {
+#pragma unroll
+      for (int bb = 0; bb < WIN; ++bb) {
+        float v[NV], o[NV];
+#pragma unroll
+        for (int t = 0; t < VPL; ++t) {
+          float4 xa = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (ok) xa = *reinterpret_cast<const float4*>(x + lidx(xl, b, ho * s + a2, wo * s + bb, c0 + 4 * t));
+          v[4 * t] = xa.x; v[4 * t + 1] = xa.y; v[4 * t + 2] = xa.z; v[4 * t + 3] = xa.w;
+        }
+        lrn_lane<VPL, false>(v, v, sl, alpha, beta, k, o);
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+          if (o[j] > best[j]) { best[j] = o[j]; bi[j] = a2 * WIN + bb; }
+      }
+    }
+    if (!ok) continue;
+#pragma unroll
+    for (int t = 0; t < VPL; ++t) {
+      const int64_t yi = lidx(yl, b, ho, wo, c0 + 4 * t);
+      *reinterpret_cast<float4*>(y + yi) = make_float4(best[4 * t], best[4 * t + 1], best[4 * t + 2], best[4 * t + 3]);
+      if (arg)
+        *reinterpret_cast<uchar4*>(arg + yi) = make_uchar4((uint8_t)bi[4 * t], (uint8_t)bi[4 * t + 1],
+                                                           (uint8_t)bi[4 * t + 2], (uint8_t)bi[4 * t + 3]);
+    }
+  }
+}
+
 // Fused MaxPool backward (stride 2) -> LRN backward (size 5) -> GradReLU, for a
 // MaxPool whose input is an LRN output (AlexNet norm1 -> pool1, norm2 -> pool2):
 // a half-warp owns one 2x2 block of pooled-from pixels, lane sl the 4*VPL contiguous
@@ -1634,6 +1690,36 @@ extern "C" int wap_maxpool_bwd(const uint8_t* argmax, const float* dy, wap_layou
     maxpool_bwd_kernel<2, 2><<<grid, 256, 0, STREAM(stream)>>>(argmax, dy, dyl, window, stride, dx, dxl, mask, ml);
   else
     maxpool_bwd_kernel<0, 0><<<grid, 256, 0, STREAM(stream)>>>(argmax, dy, dyl, window, stride, dx, dxl, mask, ml);
+  WAP_LAUNCH_CHECK();
+  COUNT_LAUNCH();
+  return WAP_OK;
+}
+
+extern "C" int wap_lrn_maxpool_fwd(const float* x, wap_layout_t xl, int size, float alpha, float beta, float bias,
+                                   int window, int stride, float* y, wap_layout_t yl, uint8_t* argmax,
+                                   void* stream) {
+  int rc;
+  if ((rc = check_layout(xl, "x")) || (rc = check_layout(yl, "y"))) return rc;
+  WAP_CHECK_ARG(size == 5 && (window == 2 || window == 3) && stride >= 1,
+                "fused lrn+maxpool forward: LRN size 5, window 2/3 only");
+  WAP_CHECK_ARG(xl.C == 64 || xl.C == 192, "fused lrn+maxpool forward: C must be 64 or 192");
+  WAP_CHECK_ARG(xl.ld == xl.C && yl.ld == xl.C, "fused lrn+maxpool forward: compact channel layouts only");
+  WAP_CHECK_ARG(yl.H == (xl.H - window) / stride + 1 && yl.W == (xl.W - window) / stride + 1 && yl.C == xl.C &&
+                    yl.B == xl.B,
+                "fused lrn+maxpool forward: output layout does not match");
+  const int64_t nout = (int64_t)yl.B * yl.H * yl.W;
+  WAP_CHECK_ARG(nout < (1LL << 31), "fused lrn+maxpool forward: too many pixels");
+  int64_t blocks = ((nout + 1) / 2 * 32 + 255) / 256;
+  if (blocks > (int64_t)WAP_NUM_SMS * 16) blocks = (int64_t)WAP_NUM_SMS * 16;
+  cudaStream_t st = STREAM(stream);
+#define WAP_LRNMP(WIN, VPL) \
+  lrn_maxpool_fwd_kernel<WIN, VPL><<<(int)blocks, 256, 0, st>>>(x, xl, alpha, beta, bias, stride, y, yl, argmax)
+  if (window == 3) {
+    if (xl.C == 64) WAP_LRNMP(3, 1); else WAP_LRNMP(3, 3);
+  } else {
+    if (xl.C == 64) WAP_LRNMP(2, 1); else WAP_LRNMP(2, 3);
+  }
+#undef WAP_LRNMP
   WAP_LAUNCH_CHECK();
   COUNT_LAUNCH();
   return WAP_OK;

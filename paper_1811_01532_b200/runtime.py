@@ -288,6 +288,7 @@ class Program:
         # MaxPool argmax owners: (input, window, stride) -> MaxPool node
         self.pool_of: dict[tuple, str] = {}
         self._pool_lrn: dict[str, tuple] = {}  # GradLRN id -> its fused GradMaxPool operands
+        self._lrn_pool: dict[str, Node] = {}  # MaxPool id -> the LRN fused into its forward
         for nid in self.order:
             n = self.node(nid)
             if n.kind is OpKind.MAX_POOL:
@@ -1108,6 +1109,19 @@ class Program:
 
     # -- pooling / LRN -------------------------------------------------------
     def _lower_pool(self, n: Node) -> None:
+        ln = self._lrn_pool.pop(n.id, None)
+        if ln is not None:
+            x = self._in(ln, ln.inputs[0])
+            y = self._out(n.id)
+            arg = self.torch.zeros(y.numel_storage(), dtype=self.torch.uint8, device=self.device)
+            self.t[f"{n.id}::argmax"] = Tensor(y.dims, y.pad, y.ld, arg, "nhwc")
+            a = ln.attrs
+            self._emit(n.id, self.L.wap_lrn_maxpool_fwd,
+                       (x.ptr, x.layout(), a["size"], C.c_float(a["alpha"]), C.c_float(a["beta"]),
+                        C.c_float(a["bias"]), n.attr("window"), n.attr("stride"), y.ptr, y.layout(),
+                        arg.data_ptr()), "LRN+MaxPool", keep=[arg],
+                       alg_bytes=self._nbytes(x, y) + self._nbytes(y) // 4)
+            return
         x = self._in(n, n.inputs[0])
         y = self._out(n.id)
         if x.ld != y.ld:
@@ -1144,7 +1158,33 @@ class Program:
                     mask.ptr if mask is not None else None, ml), "GradMaxPool",
                    alg_bytes=self._nbytes(dy, out, mask) + self._nbytes(dy) // 4)
 
+    def _lrn_pool_fusable(self, n: Node) -> str | None:
+        """The MaxPool reading this LRN's output when the pair can run as one forward
+        kernel: the LRN output is read by nothing else (GradMaxPool nodes only name it
+        as the key of the pool's argmax), is not a graph output, LRN size 5 over
+        C = 64 / 192 compact channels, window 2/3."""
+        if os.environ.get("WAP_FUSE_LRN_POOL", "1") == "0" or n.id in self.g.outputs or n.attr("size") != 5:
+            return None
+        users = self.users.get(n.id, [])
+        pools = [u for u in users if self.kind(u) is OpKind.MAX_POOL]
+        if len(pools) != 1 or any(self.kind(u) not in (OpKind.MAX_POOL, OpKind.GRAD_MAX_POOL) for u in users):
+            return None
+        pn = self.node(pools[0])
+        if pn.inputs[0] != n.id or pn.attr("window") not in (2, 3) or pn.id in self.pool_relu_fused:
+            return None
+        x, y = self.t.get(n.inputs[0]), self.t.get(n.id)
+        py = self.t.get(pn.id)
+        if x is None or y is None or py is None or x.kind != "nhwc" or x.dims[-1] not in (64, 192):
+            return None
+        if x.ld != x.dims[-1] or py.ld != x.ld:
+            return None
+        return pn.id
+
     def _lower_lrn(self, n: Node) -> None:
+        pool = self._lrn_pool_fusable(n)
+        if pool is not None:
+            self._lrn_pool[pool] = n  # emitted by _lower_pool as wap_lrn_maxpool_fwd
+            return
         x = self._in(n, n.inputs[0])
         y = self._out(n.id)
         a = n.attrs

@@ -191,3 +191,27 @@ def test_conv_direct_3x3_c3(cuda, B, H, W, pad):
     assert ((y2[:, :H, :W].double() - ref).abs().max() / ref.abs().max()).item() < 1e-6
     if pad:
         assert torch.isnan(y2[:, H:]).all() and torch.isnan(y2[:, :, W:]).all()
+
+
+@pytest.mark.parametrize("B,H,C,win,pad", [(2, 55, 64, 3, 2), (2, 27, 192, 3, 0), (1, 16, 64, 2, 1)])
+def test_lrn_maxpool_fwd_fused_matches_unfused(cuda, B, H, C, win, pad):
+    """wap_lrn_maxpool_fwd == wap_lrn_fwd followed by wap_maxpool_fwd: pooled values and
+    argmax bit for bit."""
+    L = N.lib()
+    a, beta, k, s = 1e-4, 0.75, 2.0, 2
+    Ho = (H - win) // s + 1
+    g = torch.Generator(device="cuda").manual_seed(51)
+    x = torch.zeros(B, H + pad, H + pad, C, device=cuda)
+    x[:, :H, :H] = torch.relu(torch.randn(B, H, H, C, device=cuda, generator=g) * 3)
+    xl = N.wap_layout_t(B, H, H, C, pad, C)
+    yl = N.wap_layout_t(B, Ho, Ho, C, 0, C)
+    t = torch.zeros_like(x)
+    N.check(L.wap_lrn_fwd(x.data_ptr(), xl, 5, a, beta, k, t.data_ptr(), xl, None))
+    y1 = torch.full((B, Ho, Ho, C), float("nan"), device=cuda)
+    a1 = torch.zeros(B * Ho * Ho * C, dtype=torch.uint8, device=cuda)
+    N.check(L.wap_maxpool_fwd_ex(t.data_ptr(), xl, win, s, y1.data_ptr(), yl, a1.data_ptr(), 0, None))
+    y2 = torch.full_like(y1, float("nan"))
+    a2 = torch.full_like(a1, 77)
+    N.check(L.wap_lrn_maxpool_fwd(x.data_ptr(), xl, 5, a, beta, k, win, s, y2.data_ptr(), yl, a2.data_ptr(), None))
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2) and torch.equal(a1, a2)
