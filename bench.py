@@ -330,6 +330,8 @@ def run_ours(args, rank, world, local_rank):
     # WAP's own model next to the measurement: Eq. (1) step time for
     # this d (estimate_total; additive compute + allreduce, no overlap) and estimate_power
     # (host + d * GPU power) against the measured step time and NVML board power
+    if out is None:  # ranks > 0 print nothing
+        return out, clocks
     est = tplan.plan.chosen
     pw = planner.estimate_power(tplan.plan, wl, prof)
     out["wap_model"] = {
