@@ -90,6 +90,13 @@ int wap_gemm(const wap_gemm_desc_t* desc, void* stream);
 int wap_gemm_plan_create(const wap_gemm_desc_t* desc, void** plan);
 int wap_gemm_plan_run(void* plan, void* stream);
 void wap_gemm_plan_destroy(void* plan);
+/* The launch configuration a plan resolved to, and the part of it that fixes the fp32
+ * rounding: out[0..6] = {block_n, cta_group, splits, k_chunks_per_split, window boxes,
+ * precision, n64 pair mode}. Two plans of one descriptor with equal
+ * {splits, k_chunks_per_split, precision, cta_group, pair mode, window > 0} produce bitwise-equal outputs
+ * (same per-element accumulation order); the runtime's autotuner only chooses among
+ * those, so tuning never changes results (tests/test_gemm_gpu.py). */
+int wap_gemm_plan_info(const void* plan, int64_t out[7]);
 
 /* ---- activation layout --------------------------------------------------- */
 /* Logical NHWC [B, H, W, C] stored as [B, H+pad, W+pad, ld] (ld >= C,
@@ -221,10 +228,52 @@ typedef struct {
  * contraction and CPython-3.12 compensated summation over layers, ties -> smaller d.
  * All pointers are DEVICE pointers: layers[n_layers]; flops_out[2*n_layers]
  * (fwd, bwd per layer); t_c/t_s/thr[n_devices] (NaN for non-candidates);
- * d_out[1]. algo: 0 = ring, 1 = naive all-to-all. */
+ * d_out[1]. algo: 0 = ring, 1 = naive all-to-all; OR in WAP_WAU_PLAIN_SUM to sum the
+ * per-layer terms with a plain left fold instead (the builtin sum() of CPython < 3.12,
+ * which the reference's pyproject still admits). */
+#define WAP_WAU_PLAIN_SUM 0x100
 int wap_wau_select(const wap_wau_layer_t* layers, int n_layers, int64_t global_batch, int n_devices,
                    wap_wau_profile_t profile, int algo, int64_t* flops_out, double* t_c, double* t_s,
                    double* thr, int32_t* d_out, void* stream);
+
+/* ---- fused gradient allreduce + SGD over peer memory (AllReduceSum + SgdUpdate,
+ * transform.py:551-571 / interp.py:115-119,181-182,203-204) ------------------------
+ * Every rank maps every rank's gradient arena, variable arena and flag block
+ * (peer_memory.py: cuMemCreate + POSIX-fd export, pidfd_getfd import, cuMemMap), and
+ * in NVLS mode multicast views of the two arenas (cuMulticastCreate/BindMem). One
+ * launch per gradient bucket [offset, offset + n) floats of the arenas: rank r
+ * reduces its 1/world slice (P2P: peer loads summed in ascending rank order = the
+ * reference left fold; NVLS: multimem.ld_reduce in the switch), applies
+ * w -= lr * scale * g once, and writes w to every rank's copy (P2P stores /
+ * multimem.st), between an entry and an exit flag barrier. Replicas stay bitwise
+ * equal by construction. `slot` (< WAP_AR_SLOTS) names the bucket's barrier
+ * counters; epochs live on the device, so launches replay inside CUDA graphs. A
+ * peer that never arrives sets *status = 1 after a bounded spin (no hang). */
+#define WAP_AR_MAX_RANKS 8
+#define WAP_AR_SLOTS 64
+#define WAP_AR_P2P 0
+#define WAP_AR_NVLS 1
+#define WAP_AR_FLAG_WORDS (2 * WAP_AR_SLOTS * WAP_AR_MAX_RANKS)
+typedef struct {
+  int32_t world, rank, mode, reserved;
+  float* grad[WAP_AR_MAX_RANKS];      /* gradient arena of each rank, mapped here */
+  float* var[WAP_AR_MAX_RANKS];       /* variable arena of each rank, mapped here */
+  float* grad_mc;                     /* multicast view of the gradient arenas (NVLS) */
+  float* var_mc;                      /* multicast view of the variable arenas (NVLS) */
+  uint32_t* flags[WAP_AR_MAX_RANKS];  /* WAP_AR_FLAG_WORDS barrier words of each rank */
+  uint32_t* epochs;                   /* local device counters [WAP_AR_SLOTS], zeroed */
+  uint32_t* done;                     /* local device counters [WAP_AR_SLOTS], zeroed */
+  int32_t* status;                    /* local device error word, zeroed */
+} wap_ar_group_t;
+int wap_allreduce_sgd(const wap_ar_group_t* group, int64_t offset, int64_t n, float lr, float scale, int slot,
+                      void* stream);
+
+/* Measurement only (bench.py): a tcgen05.mma kind::tf32 issue-rate probe, one CTA
+ * per SM issuing M=128 N=256 K=8 MMAs from resident shared-memory operands. Time
+ * the launch on `stream`; wap_tf32_probe_flops(iters) is the work it performs. This
+ * is the TF32 tensor-pipe peak the GEMM roofline is quoted against. */
+double wap_tf32_probe_flops(int iters);
+int wap_tf32_probe(int iters, void* stream);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,9 @@ if os.environ.get("WAP_LIB_VARIANT"):
     _LIB_PATH = _LIB_PATH.with_name(f"libwapb200_{os.environ['WAP_LIB_VARIANT']}.so")
 MAX_TAPS = 32
 POOL_RELU_FUSED = 1  # include/wap_b200.h WAP_POOL_RELU_FUSED
+AR_MAX_RANKS = 8     # WAP_AR_MAX_RANKS
+AR_SLOTS = 64        # WAP_AR_SLOTS
+AR_FLAG_WORDS = 2 * AR_SLOTS * AR_MAX_RANKS
 
 
 class NativeUnavailable(RuntimeError):
@@ -85,6 +88,13 @@ class wap_wau_profile_t(C.Structure):
                 ("allreduce_chunk_latency", C.c_double)]
 
 
+class wap_ar_group_t(C.Structure):
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("mode", C.c_int32), ("reserved", C.c_int32),
+                ("grad", C.c_void_p * AR_MAX_RANKS), ("var", C.c_void_p * AR_MAX_RANKS),
+                ("grad_mc", C.c_void_p), ("var_mc", C.c_void_p), ("flags", C.c_void_p * AR_MAX_RANKS),
+                ("epochs", C.c_void_p), ("done", C.c_void_p), ("status", C.c_void_p)]
+
+
 _lib = None
 
 
@@ -128,6 +138,7 @@ _SIGNATURES: list[tuple[str, object, list]] = [
     ("wap_gemm_plan_create", _I, [C.POINTER(wap_gemm_desc_t), C.POINTER(_P)]),
     ("wap_gemm_plan_run", _I, [_P, _P]),
     ("wap_gemm_plan_destroy", None, [_P]),
+    ("wap_gemm_plan_info", _I, [_P, C.POINTER(C.c_int64)]),
     ("wap_im2col", _I, [_P, wap_layout_t, _I, _I, _I, _I, _I, _I, _P, _I64, _P]),
     ("wap_s2d_input", _I, [_P, wap_layout_t, _I, _I, _I, _I, _P, _I, _P]),
     ("wap_conv_direct", _I, [_P, wap_layout_t, _P, _I, _I, _I, _P, _I, _P, wap_layout_t, _P, _I64, _P]),
@@ -149,6 +160,9 @@ _SIGNATURES: list[tuple[str, object, list]] = [
     ("wap_xent_fwd_bwd", _I, [_P, _I64, _P, _I64, _I, _I, _F, _P, _P, _I64, _P, _P]),
     ("wap_pack", _I, [_P, wap_layout_t, _P, _I, _P]),
     ("wap_sgd", _I, [_P, _P, _F, _P, _I64, _P]),
+    ("wap_allreduce_sgd", _I, [C.POINTER(wap_ar_group_t), _I64, _I64, _F, _F, _I, _P]),
+    ("wap_tf32_probe_flops", _D, [_I]),
+    ("wap_tf32_probe", _I, [_I, _P]),
     ("wap_wau_select", _I, [C.POINTER(wap_wau_layer_t), _I, _I64, _I, wap_wau_profile_t, _I, _P, _P,
                             _P, _P, _P, _P]),
 ]

@@ -8,6 +8,7 @@ incremental on source/header mtimes.
 
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 from concurrent.futures import ThreadPoolExecutor
@@ -46,6 +47,12 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     """Compile all kernels and link the shared library; returns its path."""
     OBJDIR.mkdir(parents=True, exist_ok=True)
     srcs = sorted(CSRC.glob("*.cu"))
+    # objects built with other flags (e.g. a diagnostic -DWAP_GEMM_TRACE build) are stale
+    # even when the sources are older: key the object dir on a hash of the command line
+    stamp = OBJDIR / "flags.sha"
+    flags_hash = hashlib.sha256(" ".join([NVCC, *ARCH, *FLAGS]).encode()).hexdigest()
+    if not stamp.exists() or stamp.read_text() != flags_hash:
+        force = True
     if force:
         for o in OBJDIR.glob("*.o"):
             o.unlink()
@@ -58,6 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
+    stamp.write_text(flags_hash)
     return LIB
 
 

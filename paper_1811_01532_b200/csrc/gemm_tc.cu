@@ -302,3 +302,16 @@ extern "C" int wap_gemm_plan_run(void* plan, void* stream) {
 }
 
 extern "C" void wap_gemm_plan_destroy(void* plan) { delete static_cast<Plan*>(plan); }
+
+extern "C" int wap_gemm_plan_info(const void* plan, int64_t out[7]) {
+  WAP_CHECK_ARG(plan != nullptr && out != nullptr, "null plan / output");
+  const Plan& p = *static_cast<const Plan*>(plan);
+  out[0] = p.bn;
+  out[1] = p.cg;
+  out[2] = p.splits;
+  out[3] = p.args.k_chunks_per_split;
+  out[4] = p.args.win_boxes;
+  out[5] = p.prec;
+  out[6] = (p.prec == 3 && p.bn == 64 && p.cg == 1 && WAP_N64_PAIR) ? 1 : 0;
+  return WAP_OK;
+}

@@ -4,7 +4,8 @@
 //   flops   workloads.py:84-117 (int64; companions each cost one forward pass)
 //   t_c     planner.py:151-160   work = (fwd+bwd)/d, eff = work/(work+knee), work/(peak*eff)
 //   t_s     planner.py:163-177   ring / naive all-to-all
-//   T(d)    planner.py:191-192   CPython >= 3.12 sum(): Neumaier compensated, first item seeds
+//   T(d)    planner.py:191-192   CPython >= 3.12 sum(): Neumaier compensated, first item seeds;
+//                                 WAP_WAU_PLAIN_SUM in `algo`: the plain left fold of CPython < 3.12
 //   d*      planner.py:233-238   min over (T, d) -> ties to the smaller d
 // Every fp64 operation is an explicit __d*_rn intrinsic so nvcc cannot contract
 // a multiply-add into an FMA (which would change the last bit).
@@ -30,10 +31,15 @@ __device__ __forceinline__ double efficiency(double work, double knee) {
 struct Neumaier {  // CPython 3.12 builtin sum() over floats (int start 0)
   double s = 0.0, c = 0.0;
   bool first = true;
+  bool plain = false;  // CPython < 3.12: sum() is a plain running left fold
   __device__ void add(double x) {
     if (first) {  // 0 + x: the int start is absorbed exactly
       s = x;
       first = false;
+      return;
+    }
+    if (plain) {
+      s = __dadd_rn(s, x);
       return;
     }
     const double t = __dadd_rn(s, x);
@@ -49,7 +55,7 @@ struct Neumaier {  // CPython 3.12 builtin sum() over floats (int start 0)
 };
 
 __global__ void wau_kernel(const wap_wau_layer_t* __restrict__ layers, int n_layers, int64_t G, int n_dev,
-                           wap_wau_profile_t prof, int algo, int64_t* __restrict__ flops_out,
+                           wap_wau_profile_t prof, int algo, bool plain_sum, int64_t* __restrict__ flops_out,
                            double* __restrict__ t_c_out, double* __restrict__ t_s_out, double* __restrict__ thr_out,
                            int32_t* __restrict__ d_out) {
   __shared__ long long s_work[kMaxLayers];   // fwd + bwd
@@ -83,6 +89,7 @@ __global__ void wau_kernel(const wap_wau_layer_t* __restrict__ layers, int n_lay
     }
     const double dd = (double)d;
     Neumaier tc, ts;
+    tc.plain = ts.plain = plain_sum;
     for (int l = 0; l < n_layers; ++l) {
       // compute_time: exact int64 -> double (values < 2^53), correctly rounded division
       const double work = __ddiv_rn((double)s_work[l], dd);
@@ -136,12 +143,14 @@ extern "C" int wap_wau_select(const wap_wau_layer_t* layers, int n_layers, int64
   WAP_CHECK_ARG(n_layers >= 0 && n_layers <= kMaxLayers, "wau: n_layers %d out of [0,%d]", n_layers, kMaxLayers);
   WAP_CHECK_ARG(n_devices >= 1 && n_devices <= kMaxDevices, "device set is empty or too large (%d)", n_devices);
   WAP_CHECK_ARG(global_batch >= 1, "wau: global batch must be positive");
+  const bool plain_sum = (algo & WAP_WAU_PLAIN_SUM) != 0;
+  algo &= ~WAP_WAU_PLAIN_SUM;
   WAP_CHECK_ARG(algo == 0 || algo == 1, "unknown aggregation algorithm %d", algo);
   WAP_CHECK_ARG(profile.peak_flops > 0 && profile.link_bandwidth > 0, "wau: bad profile");
   WAP_CHECK_ARG(layers || n_layers == 0, "wau: null layers");
   WAP_CHECK_ARG(flops_out && t_c && t_s && thr && d_out, "wau: null output");
   wau_kernel<<<1, 64, 0, reinterpret_cast<cudaStream_t>(stream)>>>(layers, n_layers, global_batch, n_devices, profile,
-                                                                   algo, flops_out, t_c, t_s, thr, d_out);
+                                                                   algo, plain_sum, flops_out, t_c, t_s, thr, d_out);
   WAP_LAUNCH_CHECK();
   g_wap_launches.fetch_add(1, std::memory_order_relaxed);
   return WAP_OK;

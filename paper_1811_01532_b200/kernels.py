@@ -62,6 +62,22 @@ class GemmCall:
     def __call__(self, stream=None):
         N.check(N.lib().wap_gemm_plan_run(self._plan, N.stream_ptr(stream)), "wap_gemm_plan_run")
 
+    def info(self) -> dict:
+        """The resolved launch configuration (wap_gemm_plan_info)."""
+        out = (C.c_int64 * 7)()
+        N.check(N.lib().wap_gemm_plan_info(self._plan, out), "wap_gemm_plan_info")
+        return dict(zip(("block_n", "cta_group", "splits", "k_chunks_per_split", "window_boxes", "precision",
+                         "pair"), (int(v) for v in out)))
+
+    def numerics(self) -> tuple:
+        """What fixes the fp32 rounding of the result: K split, precision, CTA group,
+        N = 64 pair mode, halo window (it walks K tap-innermost, the plain plan
+        tap-outermost). Measured on B200: plans equal in these are bitwise equal
+        (tests/test_determinism_gpu.py); BN does not enter."""
+        i = self.info()
+        return (i["splits"], i["k_chunks_per_split"] if i["splits"] > 1 else 0, i["precision"], i["cta_group"],
+                i["pair"], int(i["window_boxes"] > 0))
+
     def __del__(self):
         try:
             if self._plan:

@@ -151,12 +151,16 @@ class Program:
     precision:    3 = 3xTF32 (fp32-accurate, default), 1 = TF32.
     in_place:     SgdUpdate overwrites the variable buffers (training loop);
                   otherwise updates go to fresh output buffers (execute()).
-    collective:   callable(list[(offset, numel)] , arena_tensor) performing the
-                  cross-rank SUM of gradient slices (None: single process).
+    collective:   callable(arena slice) performing the cross-rank SUM of a
+                  gradient bucket in place (NCCL / gloo; None: single process).
+    fused:        a peer_memory.FusedAllReduce: the variable / gradient arenas
+                  live in peer-mapped memory and every bucket's allreduce + SGD
+                  is ONE wap_allreduce_sgd launch (replaces `collective`).
     """
 
     def __init__(self, graph: Graph, precision: int = 3, device=None, in_place: bool = False,
-                 collective=None, bucket_bytes: int = 64 << 20, autotune: bool | None = None):
+                 collective=None, bucket_bytes: int = 64 << 20, autotune: bool | None = None, fused=None,
+                 collective_capturable: bool = False):
         import torch
 
         import os
@@ -177,6 +181,10 @@ class Program:
         self.precision = precision
         self.in_place = in_place
         self.collective = collective
+        self.collective_capturable = collective_capturable  # NCCL: recordable into the step's CUDA graph
+        self.fused = fused
+        if fused is not None and (collective is not None or not in_place):
+            raise EvalError("the fused allreduce + SGD needs an in-place training program and no other collective")
         self.t: dict[str, Tensor] = {}
         self.steps: list = []
         self.update_steps: list = []
@@ -480,8 +488,13 @@ class Program:
             self.arena_off[v] = off
             off += sizes[v]
         self.arena_numel = max(off, 4)
-        self.var_arena = torch.zeros(self.arena_numel, dtype=torch.float32, device=self.device)
-        self.grad_arena = torch.zeros(self.arena_numel, dtype=torch.float32, device=self.device)
+        if self.fused is not None:
+            # peer-mapped (and multicast) arenas: every rank's fused allreduce + SGD
+            # reads our gradients and writes our variables directly
+            self.var_arena, self.grad_arena = self.fused.allocate(self.arena_numel)
+        else:
+            self.var_arena = torch.zeros(self.arena_numel, dtype=torch.float32, device=self.device)
+            self.grad_arena = torch.zeros(self.arena_numel, dtype=torch.float32, device=self.device)
         for v in self.var_ids:
             d = self.dims(v)
             o = self.arena_off[v]
@@ -678,21 +691,43 @@ class Program:
             raise EvalError(f"no GPU rule for kind {k.value}")
 
     def _autotune_gemms(self, reps: int = 3) -> None:
-        """Per-GEMM launch configuration by measurement: one CTA vs a CTA pair
-        (cta_group::2), each with its own split-K choice. Buffers are already
-        allocated; timings are data-independent."""
+        """Per-GEMM launch configuration: one CTA vs a CTA pair (cta_group::2), halo
+        window on/off, BN = 128 vs wide tiles, explicit K splits for FC GEMMs.
+
+        Results never depend on the run (plan_cache.py): a GEMM whose descriptor is
+        in the committed plan file takes that configuration without timing; otherwise
+        only candidates with the automatic plan's numerics signature (same K split
+        and MMA pairing, hence the same accumulation order per element) are timed.
+        WAP_AUTOTUNE_FREE=1 lifts the restriction (tools/tune_plans.py uses it to
+        write the plan file). Buffers are already allocated; timings are
+        data-independent."""
+        from . import plan_cache
         from .kernels import GemmCall
 
         torch = self.torch
         stream = torch.cuda.current_stream(self.device)
         s = N.stream_ptr()
+        free = os.environ.get("WAP_AUTOTUNE_FREE") == "1"
+        self.tuned_plans: dict[str, dict] = {}
         for st in self.steps + self.update_steps:
             if not isinstance(st, _GemmStep):
+                continue
+            key = plan_cache.key(st.desc)
+            pinned = None if free else plan_cache.lookup(st.desc)
+            if pinned is not None:
+                d = type(st.desc).from_buffer_copy(st.desc)
+                d.cluster, d.window, d.block_n = pinned["cluster"], pinned["window"], pinned["block_n"]
+                d.splits = pinned["splits"]
+                d.workspace, d.workspace_bytes = None, 0
+                st.call = GemmCall(d, device=self.device)
+                st.tuned_ms, st.plan_src = None, "plan file"
+                self.tuned_plans[key] = dict(pinned)
                 continue
             small_m = st.desc.M <= 128
             if small_m and os.environ.get("WAP_AUTOTUNE_FC", "1") == "0":
                 continue
-            best, best_ms = st.call, None
+            sig = st.call.numerics()
+            best, best_ms, best_choice = st.call, None, None
             a = st.desc.a
             windows = (0, -1) if (self.precision == 3 and not a.mn_major and a.ntaps > 1) else (0,)
             # BN = 128 keeps two TMEM accumulators in 3xTF32 (epilogue overlaps the next tile),
@@ -726,6 +761,8 @@ class Program:
                     call = GemmCall(d, device=self.device)
                 except Exception:
                     continue
+                if not free and call.numerics() != sig:
+                    continue
                 N.check(self.L.wap_gemm_plan_run(call._plan, s), "autotune warm-up")
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -736,11 +773,15 @@ class Program:
                 ms = e0.elapsed_time(e1) / reps
                 if os.environ.get("WAP_AUTOTUNE_LOG"):
                     print(f"autotune {st.name} M={d.M} N={d.N} K={d.K} cluster={cluster} window={window} bn={bn} "
-                          f"splits={sp} {ms:.4f} ms", flush=True)
+                          f"splits={sp} sig={call.numerics()} {ms:.4f} ms", flush=True)
                 if best_ms is None or ms < best_ms:
                     best, best_ms = call, ms
+                    best_choice = {"cluster": cluster, "window": window, "block_n": bn, "splits": d.splits}
             st.call = best
             st.tuned_ms = best_ms
+            st.plan_src = "autotune (free)" if free else "autotune (numerics-preserving)"
+            if best_choice is not None:
+                self.tuned_plans[key] = best_choice
 
     def _schedule_collectives(self) -> None:
         """Bucket the rank-local gradient allreduces and overlap them with backward.
@@ -770,6 +811,9 @@ class Program:
         side = self.torch.cuda.Stream(device=self.device)
         self.comm_stream = side
         inserts: dict[int, list] = {}
+        if self.fused is not None:
+            self._schedule_fused(buckets, side, inserts)
+            return
         # SGD of a bucket also runs on the comm stream, right behind its allreduce,
         # once the last backward kernel reading those weights (GradMatMulX /
         # GradConv2DX) has been issued: the update overlaps the rest of backward.
@@ -779,7 +823,8 @@ class Program:
         for ready, lo, hi, ids in buckets:
             buf = self.grad_arena[lo:hi]
             inserts.setdefault(ready, []).append(
-                _BucketStep("+".join(ids), self.collective, buf, side, self.torch, self.par_stream))
+                _BucketStep("+".join(ids), self.collective, buf, side, self.torch, self.par_stream,
+                            self.collective_capturable))
             if self.bucket_sgd:
                 vars_in = [v for o, v in var_of_slot.items() if lo <= o < hi]
                 readers = [self.step_end[u] for v in vars_in for u in self.users[v]
@@ -797,6 +842,37 @@ class Program:
         new_steps.extend(inserts.get(len(self.steps), []))
         new_steps.append(_JoinStep(side, self.torch))
         self.steps = new_steps
+        self.buckets = [(lo * 4, hi * 4, ids) for _, lo, hi, ids in buckets]
+
+    def _schedule_fused(self, buckets, side, inserts) -> None:
+        """One wap_allreduce_sgd per bucket on the comm stream: reduce-scatter +
+        SGD + all-gather over peer memory (csrc/allreduce.cu). It writes every
+        rank's copy of the bucket's variables, so it goes where the bucket SGD
+        would: behind the bucket's last gradient AND the last backward kernel
+        reading those weights; the kernel's entry barrier extends that to all ranks."""
+        from . import _native as N
+
+        lr = self._uniform_lr()
+        if lr is None:
+            raise EvalError("the fused allreduce + SGD needs one learning rate for every variable")
+        if len(buckets) > N.AR_SLOTS:
+            raise EvalError(f"{len(buckets)} buckets exceed the {N.AR_SLOTS} barrier slots; raise bucket_bytes")
+        var_of_slot = {self.arena_off[v]: v for v in self.arena_off}
+        for slot, (ready, lo, hi, ids) in enumerate(buckets):
+            vars_in = [v for o, v in var_of_slot.items() if lo <= o < hi]
+            readers = [self.step_end[u] for v in vars_in for u in self.users[v]
+                       if self.kind(u) is not OpKind.SGD_UPDATE]
+            at = max([ready] + readers)
+            inserts.setdefault(at, []).append(
+                _FusedBucketStep("+".join(ids), self.fused, lo, hi - lo, lr, slot, side, self.torch, self.par_stream))
+        new_steps = []
+        for i, st in enumerate(self.steps):
+            new_steps.extend(inserts.get(i, []))
+            new_steps.append(st)
+        new_steps.extend(inserts.get(len(self.steps), []))
+        new_steps.append(_JoinFused(side, self.torch))
+        self.steps = new_steps
+        self.bucket_sgd = True
         self.buckets = [(lo * 4, hi * 4, ids) for _, lo, hi, ids in buckets]
 
     def _uniform_lr(self):
@@ -1244,13 +1320,15 @@ class Program:
         for t in ins:
             if t.numel_storage() != out.numel_storage() or t.ld != out.ld or t.pad != out.pad:
                 raise EvalError(f"{n.id!r}: AddN operands must share one layout")
-        for lo in range(0, len(ins), 16):
-            chunk = ins[lo:lo + 16]
-            srcs = ([out] if lo else []) + chunk
-            srcs = srcs[:16]
+        # wap_add_n folds at most 16 sources left to right (interp.py:115-119): the first
+        # launch takes ins[0:16], every later one the running sum plus the next 15 operands
+        lo = 0
+        while lo < len(ins):
+            srcs = ins[0:16] if lo == 0 else [out] + ins[lo:lo + 15]
             arr = (C.c_void_p * len(srcs))(*[t.ptr for t in srcs])
             self._emit(f"{n.id}#{lo}", self.L.wap_add_n, (arr, len(srcs), out.layout(), out.ptr), "AddN",
                        keep=[arr])
+            lo += len(srcs) - (0 if lo == 0 else 1)
 
     def _lower_allreduce(self, n: Node) -> None:
         if len(n.inputs) >= 2:  # all replicas in this process: left fold (interp.py:181-182)
@@ -1259,7 +1337,7 @@ class Program:
         # rank-local view: the sum crosses processes. Recorded here, bucketed in
         # _schedule_collectives once every producer's position is known.
         src = self._in(n, n.inputs[0])
-        if self.collective is not None:
+        if self.collective is not None or self.fused is not None:
             self._collectives.append((len(self.steps), n.id, src))
 
     def _lower_concat(self, n: Node) -> None:
@@ -1296,13 +1374,15 @@ class Program:
     def capture(self) -> None:
         """Record the whole step as one CUDA graph (replayed by run())."""
         torch = self.torch
-        if any(isinstance(s, _CollectiveStep) for s in self.steps):
-            raise EvalError("steps with cross-process collectives are not captured")
+        if any(isinstance(s, _CollectiveStep) and not s.capturable for s in self.steps):
+            raise EvalError("steps with non-capturable (gloo) collectives are not captured")
         side = torch.cuda.Stream(device=self.device)
-        side.wait_stream(torch.cuda.current_stream(self.device))
         # the warm-up pass is a real training step (in-place SGD): keep the variables
-        # as they were, so capture() + the first replay is exactly one step
+        # as they were, so capture() + the first replay is exactly one step. The
+        # snapshot is queued before the side stream forks, so the warm-up's in-place
+        # update is ordered after it.
         saved = self.var_arena.clone() if self.in_place else None
+        side.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(side):
             for st in self.steps:  # warm-up on the capture stream
                 st(N.stream_ptr(side))
@@ -1323,8 +1403,8 @@ class Program:
         called with the capture stream's pointer). No warm-up: capture() already ran
         one, so kernels are loaded and GEMM plans tuned."""
         torch = self.torch
-        if any(isinstance(s, _CollectiveStep) for s in self.steps):
-            raise EvalError("steps with cross-process collectives are not captured")
+        if any(isinstance(s, _CollectiveStep) and not s.capturable for s in self.steps):
+            raise EvalError("steps with non-capturable (gloo) collectives are not captured")
         side = torch.cuda.Stream(device=self.device)
         side.wait_stream(torch.cuda.current_stream(self.device))
         g = torch.cuda.CUDAGraph()
@@ -1503,11 +1583,16 @@ def name_out_of(prog, buf) -> str | None:
 
 
 class _CollectiveStep:
-    """Marker base for steps that call into a cross-process collective."""
+    """Marker base for steps that call into a cross-process collective.
+    `capturable`: the step can be recorded into a CUDA graph (event waits, our
+    kernels, NCCL); a gloo collective cannot."""
+
+    capturable = True
 
 
 class _BucketStep(_CollectiveStep):
-    def __init__(self, name, fn, buf, side, torch, par=None):
+    def __init__(self, name, fn, buf, side, torch, par=None, capturable=False):
+        self.capturable = capturable
         self.name = name
         self.fn = fn
         self.buf = buf
@@ -1577,6 +1662,39 @@ class _SideStep(_CollectiveStep):
         from . import _native as N
 
         self.step(N.stream_ptr(self.side))
+
+
+class _FusedBucketStep:
+    """wap_allreduce_sgd of one gradient bucket on the comm stream, after the
+    compute stream reaches this point and the weight-gradient stream drained.
+    Capturable: event waits plus one kernel launch."""
+
+    def __init__(self, name, fused, offset, n, lr, slot, side, torch, par=None):
+        self.name = f"allreduce_sgd[{name}]"
+        self.fused, self.offset, self.n, self.lr, self.slot = fused, offset, n, lr, slot
+        self.side, self.torch, self.par = side, torch, par
+        self.alg_bytes = 12 * n  # local grad read + var read + var write (peer traffic on NVLink)
+
+    def __call__(self, stream: int) -> None:
+        torch = self.torch
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.side.wait_event(ev)
+        if self.par is not None:
+            self.side.wait_stream(self.par)
+        from . import _native as N
+
+        self.fused.launch(self.offset, self.n, self.lr, self.slot, N.stream_ptr(self.side))
+
+
+class _JoinFused:
+    def __init__(self, side, torch):
+        self.name = "join(comm)"
+        self.side = side
+        self.torch = torch
+
+    def __call__(self, stream: int) -> None:
+        self.torch.cuda.current_stream().wait_stream(self.side)
 
 
 class _JoinStep(_CollectiveStep):

@@ -98,13 +98,23 @@ class Trainer:
 
     `step(images, labels)` takes this rank's shard (host or device arrays; host
     arrays are copied H2D inside the call) and returns the rank's loss (a
-    device scalar unless fetch=True). Gradients are summed across ranks with
-    torch.distributed (NCCL) when world_size > 1; the loss seed already divides
-    by the global batch, so no 1/N scaling is needed (training.py:94-102)."""
+    device scalar unless fetch=True). With world_size > 1 the gradients are summed
+    across ranks per bucket, overlapping the rest of backward, by
+      allreduce="nccl": torch.distributed all_reduce (NCCL over NVLink) on a comm
+                        stream, each bucket's SGD behind it;
+      allreduce="p2p":  one fused wap_allreduce_sgd kernel per bucket over
+                        peer-mapped memory (left fold in rank order = the
+                        reference's AllReduceSum, then SGD, then all-gather);
+      allreduce="nvls": the same kernel with multimem.ld_reduce / multimem.st
+                        through the NVSwitch.
+    (default: $WAP_ALLREDUCE, else "nccl"). The loss seed already divides by the
+    global batch, so no 1/N scaling is needed (training.py:94-102). The whole
+    step is one CUDA graph whenever its collectives are capturable (d == 1,
+    NCCL, or the fused kernel; not gloo)."""
 
     def __init__(self, tplan: TrainingPlan, rank: int = 0, precision: int = 3, seed: int = 0,
                  variables: dict | None = None, process_group=None, use_graph: bool = True,
-                 bucket_bytes: int = 64 << 20):
+                 bucket_bytes: int = 64 << 20, allreduce: str | None = None):
         import torch
 
         from .interp import initial_variables
@@ -116,9 +126,21 @@ class Trainer:
         self.rank = rank
         self.view = rank_view(tplan.graph, rank, self.d)
         self.pg = process_group
-        collective = self._allreduce if self.d > 1 else None
+        self.allreduce = allreduce or os.environ.get("WAP_ALLREDUCE", "nccl")
+        if self.allreduce not in ("nccl", "p2p", "nvls"):
+            raise TransformError(f"unknown allreduce {self.allreduce!r} (nccl, p2p, nvls)")
+        collective, fused, capturable = None, None, True
+        if self.d > 1 and self.allreduce == "nccl":
+            import torch.distributed as dist
+
+            collective = self._allreduce
+            capturable = dist.get_backend(self.pg) == "nccl"
+        elif self.d > 1:
+            from .peer_memory import FusedAllReduce
+
+            fused = FusedAllReduce(rank, self.d, torch.cuda.current_device(), self.allreduce, self.pg)
         self.prog = Program(self.view, precision=precision, in_place=True, collective=collective,
-                            bucket_bytes=bucket_bytes)
+                            bucket_bytes=bucket_bytes, fused=fused, collective_capturable=capturable)
         init = initial_variables(self.view, seed)
         if variables:
             for k in init:
@@ -130,7 +152,7 @@ class Trainer:
         self.prog.bind(init)
         self.inputs = [n.id for n in self.view if n.kind is OpKind.INPUT]
         self.loss_id = next(o for o in self.view.outputs if self.view.node(o).kind is OpKind.SOFTMAX_XENT_LOSS)
-        self.use_graph = use_graph and self.d == 1
+        self.use_graph = use_graph and capturable
         self._captured = False
 
     def _allreduce(self, buf) -> None:

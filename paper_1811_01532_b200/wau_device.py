@@ -9,6 +9,7 @@ current CUDA device and returns (d, [CostEstimate...]) in candidate order.
 from __future__ import annotations
 
 import ctypes as C
+import sys
 
 from . import _native as N
 from .errors import WorkloadError
@@ -17,6 +18,9 @@ from .planner import CostEstimate, DeviceProfile
 from .workloads import NetworkWorkload
 
 ALGO_CODES = {"ring": 0, "naive_all_to_all": 1}
+# planner.py:191-192 sums with the builtin sum(): Neumaier-compensated from CPython 3.12
+# on, a plain left fold before. The device kernel follows the interpreter it runs under.
+PLAIN_SUM = 0x100 if sys.version_info < (3, 12) else 0
 
 
 def layer_descriptors(graph: Graph) -> tuple[list[N.wap_wau_layer_t], int]:
@@ -94,7 +98,7 @@ def run(records, G: int, n_devices: int, profile: DeviceProfile, algo: str = "ri
                                profile.link_latency, profile.allreduce_chunk_latency)
     with torch.cuda.device(dev):
         N.check(N.lib().wap_wau_select(C.cast(C.c_void_p(d_layers.data_ptr()), C.POINTER(N.wap_wau_layer_t)),
-                                       n, G, n_devices, prof, ALGO_CODES[algo], flops.data_ptr(),
+                                       n, G, n_devices, prof, ALGO_CODES[algo] | PLAIN_SUM, flops.data_ptr(),
                                        t_c.data_ptr(), t_s.data_ptr(), thr.data_ptr(), d_out.data_ptr(),
                                        N.stream_ptr()), "wap_wau_select", WorkloadError)
         torch.cuda.current_stream().synchronize()

@@ -66,3 +66,23 @@ def test_product_path_has_no_cpu_fallback():
 
     with pytest.raises(N.NativeUnavailable):
         Program(models.mlp(8))
+
+
+def test_allreduce_sgd_rejects_bad_groups_without_gpu():
+    """wap_allreduce_sgd validates the group before any launch (no device needed)."""
+    L = N.lib()
+    assert L.wap_allreduce_sgd(None, 0, 4, C.c_float(0.1), C.c_float(1.0), 0, None) == -1
+    g = N.wap_ar_group_t()
+    g.world, g.rank = 0, 0
+    assert L.wap_allreduce_sgd(C.byref(g), 0, 4, C.c_float(0.1), C.c_float(1.0), 0, None) == -1
+    assert b"world" in L.wap_last_error()
+    g.world, g.rank = 2, 2
+    assert L.wap_allreduce_sgd(C.byref(g), 0, 4, C.c_float(0.1), C.c_float(1.0), 0, None) == -1
+    g.rank = 0
+    assert L.wap_allreduce_sgd(C.byref(g), 0, 4, C.c_float(0.1), C.c_float(1.0), N.AR_SLOTS, None) == -1
+    assert b"slot" in L.wap_last_error()
+    # counters present but rank 1's buffers not mapped
+    g.epochs = g.done = g.status = 16
+    assert L.wap_allreduce_sgd(C.byref(g), 0, 4, C.c_float(0.1), C.c_float(1.0), 0, None) == -1
+    assert b"not mapped" in L.wap_last_error()
+    assert C.sizeof(N.wap_ar_group_t) == 16 + 8 * (3 * N.AR_MAX_RANKS + 5)

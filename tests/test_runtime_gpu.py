@@ -125,3 +125,19 @@ def test_device_wau_matches_host_planner(cuda):
         w = workloads.extract_workloads(g)
         plan = planner.select_parallelism_device(w, tuple(range(8)), profs[c["profile"]], c["algo"])
         assert plan.d == c["d"] and plan.predicted_power.hex() == c["power"]
+
+
+@pytest.mark.parametrize("n_ops", [2, 16, 17, 31, 32, 33, 47, 48, 50])
+def test_add_n_many_operands_left_fold(cuda, n_ops):
+    """AddN over more operands than one wap_add_n launch folds (16): every operand
+    enters the sum (interp.py:115-119 left fold), checked against the oracle."""
+    b = ir.GraphBuilder("addn")
+    ids = [b.input(f"x{i}", (3, 5)) for i in range(n_ops)]
+    b.add(ir.OpKind.ADD_N, "s", ids)
+    b.output("s")
+    g = b.build()
+    rs = np.random.default_rng(n_ops)
+    bind = {i: rs.standard_normal((3, 5)) for i in ids}
+    got = interp.execute(g, bind, seed=0)["s"]
+    ref = O.left_fold([bind[i].astype(np.float32).astype(np.float64) for i in ids])
+    assert O.relative_deviation(got, ref) < 1e-6
