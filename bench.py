@@ -239,6 +239,12 @@ def run_ours(args, model, rank, world, local_rank, tf32_peak):
         return float(t.item())
 
     clk = ClockSampler(local_rank).start()
+    # idle board power (profile calibration: power_idle), before this network's work
+    torch.cuda.synchronize()
+    time.sleep(0.5)
+    i0 = time.time()
+    time.sleep(1.5)
+    idle_window = (i0, time.time())
     for _ in range(args.warmup):
         tr.run()
     barrier()
@@ -289,6 +295,7 @@ def run_ours(args, model, rank, world, local_rank, tf32_peak):
     clocks = clk.summary(timed_window)
     # drop the first second (the NVML average still carries the pre-window level)
     pw = clk.summary((p0 + 1.0, p1))
+    idle = clk.summary(idle_window)
     barrier()
 
     # ---- instrumented pass: per-launch CUDA events over the same step ----
@@ -331,6 +338,12 @@ def run_ours(args, model, rank, world, local_rank, tf32_peak):
         return None
     est = tplan.plan.chosen
     pw_pred = planner.estimate_power(tplan.plan, wl, prof)
+    # estimate_power's GPU term is idle + (peak - idle) * util (planner.py:198-214 of the
+    # reference): the power_peak that reproduces the measured load power at this util
+    util = ((pw_pred - prof.host_power) / tplan.plan.d - prof.power_idle) / (prof.power_peak - prof.power_idle)
+    fit_peak = None
+    if pw["power_w"] and idle["power_w"] and util > 0:
+        fit_peak = round(idle["power_w"] + (pw["power_w"] - idle["power_w"]) / util, 1)
     return {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
@@ -384,6 +397,8 @@ def run_ours(args, model, rank, world, local_rank, tf32_peak):
             "predicted_power_w": round(pw_pred, 1),
             "predicted_gpu_power_w": round((pw_pred - prof.host_power) / tplan.plan.d, 1),
             "measured_gpu_power_w": pw["power_w"],
+            "measured_idle_power_w": idle["power_w"], "model_util": round(util, 4),
+            "fitted_power_peak_w": fit_peak,
             "power_window": {"seconds": round(p1 - p0, 2), "steps": n_pw, "samples": pw["samples"],
                              "sm_mhz": pw["sm_mhz"], "reasons": pw["reasons"]},
             "profile": prof.name,

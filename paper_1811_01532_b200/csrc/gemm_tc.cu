@@ -86,12 +86,18 @@ int make_tmap(CUtensorMap* tm, const wap_operand_t& op, int box_outer) {
 
 int pick_bn(const wap_gemm_desc_t& d) {
   if (d.block_n) return d.block_n;
-  const int64_t ntiles = (d.N + 255) / 256;
+  // 3xTF32 with split accumulators holds 2 x BN accumulator columns next to the TMEM
+  // A slots: BN <= 192
+  const int widest = (d.precision == 3 && WAP_SPLIT_ACC) ? 192 : 256;
+  const int64_t ntiles = (d.N + widest - 1) / widest;
   const int64_t per = (d.N + ntiles - 1) / ntiles;
   for (int bn : {64, 128, 192, 256})
     if (per <= bn) return bn;
   return 256;
 }
+
+constexpr int kMaxChainChunks = 64;               // 2048 K per accumulator chain
+constexpr long long kAccSlabBytes = 64LL << 20;   // split-K workspace the accuracy rule may use
 
 struct Shape {
   int bn, cg, splits, kps, m_tiles, n_tiles, k_chunks;
@@ -121,6 +127,19 @@ Shape plan_shape(const wap_gemm_desc_t& d) {
     splits = (int)std::max(1LL, slots / tiles);
     splits = std::min(splits, std::max(1, s.k_chunks / 8));
   }
+  // accuracy: the tcgen05 accumulator rounds toward zero, about one ulp per MMA
+  // (tools/gemm_split_acc.py), so a long K chain drifts (-6.7e-9 x K relative).
+  // Automatic plans cut chains longer than kMaxChainChunks into slabs (summed in
+  // round-to-nearest fp32 by the deterministic reduction) whenever the slabs are
+  // cheap: weight gradients and other small-output / long-K GEMMs.
+  if (d.splits <= 0 && !(d.mbits_out || d.mbits_in)) {
+    const int need = wap_ceil_div(s.k_chunks, kMaxChainChunks);
+    if (need > splits) {
+      const long long per_slab = (long long)d.M * d.ldc * 4;
+      const long long cap = std::max(1LL, kAccSlabBytes / std::max(1LL, per_slab));
+      splits = (int)std::max<long long>(splits, std::min<long long>(need, cap));
+    }
+  }
   splits = std::max(1, std::min(splits, s.k_chunks));
   s.kps = wap_ceil_div(s.k_chunks, splits);
   s.splits = wap_ceil_div(s.k_chunks, s.kps);
@@ -132,8 +151,12 @@ int win_smem_cg(int bn, int boxes) {
   switch (bn) {
     case 64: return smem_bytes_for<64, 3, CG, true>(boxes);
     case 128: return smem_bytes_for<128, 3, CG, true>(boxes);
+#if WAP_SPLIT_ACC
+    default: return smem_bytes_for<192, 3, CG, true>(boxes);  // 3xTF32: BN <= 192
+#else
     case 192: return smem_bytes_for<192, 3, CG, true>(boxes);
     default: return smem_bytes_for<256, 3, CG, true>(boxes);
+#endif
   }
 }
 
@@ -180,6 +203,7 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
   if ((rc = validate_operand(d.a, "a")) || (rc = validate_operand(d.b, "b"))) return rc;
   const Shape s = plan_shape(d);
   WAP_CHECK_ARG(s.bn == 64 || s.bn == 128 || s.bn == 192 || s.bn == 256, "block_n must be 64/128/192/256");
+  WAP_CHECK_ARG(!(d.precision == 3 && WAP_SPLIT_ACC && s.bn > 192), "3xTF32 tiles are at most 192 columns wide");
   if ((rc = make_tmap(&p->tmA, d.a, d.a.mn_major ? BK : BM))) return rc;
   if ((rc = make_tmap(&p->tmB, d.b, d.b.mn_major ? BK : s.bn / s.cg))) return rc;
   GemmArgs& g = p->args;

@@ -45,6 +45,17 @@ constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap
 #ifndef WAP_N64_PAIR
 #define WAP_N64_PAIR 1
 #endif
+// Split accumulators (3xTF32): the tcgen05 MMA rounds its accumulator toward zero,
+// about one ulp of the accumulator per MMA (tools/gemm_split_acc.py: bias
+// -6.7e-9 * K relative, linear in the MMAs per accumulator, for exact-in-tf32
+// inputs). Adding the two small cross products into the same accumulator as
+// big*big triples the truncation events (measured: 3.6x the exact-input bias).
+// With WAP_SPLIT_ACC each accumulator has a second half: big*big goes to half 0,
+// small*B and A*small to half 1 (2^-10 smaller, so its truncations are
+// negligible), and the epilogue adds the halves in round-to-nearest fp32.
+#ifndef WAP_SPLIT_ACC
+#define WAP_SPLIT_ACC 1
+#endif
 // fewest TMEM A slots (3xTF32) worth keeping two accumulators for
 #ifndef WAP_MIN_A_SLOTS
 #define WAP_MIN_A_SLOTS 4
@@ -109,7 +120,10 @@ struct Cfg {
   // stage into a 128-column accumulator, and small*big as an N = 64 MMA into its
   // first half; the epilogue adds the two halves. 2 MMAs per k-slice instead of 3.
   static constexpr bool PAIR = PREC == 3 && BN == 64 && CG == 1 && WAP_N64_PAIR;
-  static constexpr int ACC_W = PAIR ? 128 : BN;  // TMEM columns per accumulator
+  // SACC: two-half accumulators (big*big | small products); PAIR always has two halves
+  static constexpr bool SACC = PREC == 3 && !PAIR && WAP_SPLIT_ACC;
+  static constexpr int HALF = PAIR ? 64 : BN;                      // column offset of half 1
+  static constexpr int ACC_W = PAIR ? 128 : (SACC ? 2 * BN : BN);  // TMEM columns per accumulator
   static constexpr int ACC_BUFS = (PREC == 3 && 512 - 2 * ACC_W < WAP_MIN_A_SLOTS * 64) ? 1 : 2;
   static constexpr int A_COL0 = ACC_BUFS * ACC_W;
   static constexpr int TMEM_A_SLOTS = PREC == 3 ? (512 - A_COL0) / 64 : 64;
@@ -143,6 +157,7 @@ struct Cfg {
   static_assert(PREC != 3 || !WAP_RING_EVEN || (STAGES % kSplitGroups == 0 && A_SLOTS % kSplitGroups == 0),
                 "3xTF32 rings must be multiples of the splitter group count");
   static_assert(B_ROWS % 32 == 0, "B rows per CTA must be a multiple of 32");
+  static_assert(PREC != 3 || A_SLOTS >= kSplitGroups, "3xTF32 needs TMEM A slots next to the accumulators");
 };
 
 // A row m (32 k-values) of a landed stage, K-major SWIZZLE_128B tile.
@@ -756,7 +771,15 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
                 constexpr uint32_t idesc2 = make_idesc_tf32(BM, 128, false, B_MN);
                 const uint32_t a_big = a_big0 + kk * 8;
                 umma_ts_cg<CG>(dacc, a_big, bd, idesc2, first);            // A * [B | B_small]
-                umma_ts_cg<CG>(dacc, a_big + 32, bd, idesc, 1u);           // small * B
+                if constexpr (WAP_SPLIT_ACC)
+                  umma_ts_cg<CG>(dacc + 64, a_big + 32, bd, idesc, 1u);    // small * B -> small half
+                else
+                  umma_ts_cg<CG>(dacc, a_big + 32, bd, idesc, 1u);         // small * B
+              } else if constexpr (C::SACC) {
+                const uint32_t a_big = a_big0 + kk * 8;
+                umma_ts_cg<CG>(dacc + C::HALF, a_big + 32, bd, idesc, first);  // small * B -> half 1
+                umma_ts_cg<CG>(dacc + C::HALF, a_big, bsd0 + kk * kB, idesc, 1u);  // A * small -> half 1
+                umma_ts_cg<CG>(dacc, a_big, bd, idesc, first);                 // big * big -> half 0
               } else if constexpr (PREC == 3) {
                 const uint32_t a_big = a_big0 + kk * 8;
                 umma_ts_cg<CG>(dacc, a_big + 32, bd, idesc, first);        // small * B
@@ -859,12 +882,13 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         uint32_t v[32];
         EPI_T0();
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * C::ACC_W + cb * 32, v);
-        if constexpr (C::PAIR) {
-          // second half of the pair accumulator (A * B_small), 16 columns at a time
+        if constexpr (C::PAIR || C::SACC) {
+          // second half of the accumulator (the small products), 16 columns at a time
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             uint32_t v2[16];
-            tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * C::ACC_W + 64 + cb * 32 + hh * 16, v2);
+            tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * C::ACC_W + C::HALF + cb * 32 + hh * 16,
+                               v2);
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 16; ++j)

@@ -77,6 +77,9 @@ class PeerArena:
         self.cu = cu
         self.rank, self.world, self.device = rank, world, device
         self.dev = _ck(cu.cuDeviceGet(device), "cuDeviceGet")
+        # the device's primary context: the one torch and the native library run in
+        self._ctx = _ck(cu.cuDevicePrimaryCtxRetain(self.dev), "cuDevicePrimaryCtxRetain")
+        _ck(cu.cuCtxSetCurrent(self._ctx), "cuCtxSetCurrent")
         prop = cu.CUmemAllocationProp()
         prop.type = cu.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
         prop.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE

@@ -14,6 +14,10 @@ The check is split in two, each against a stated bound:
    oracle's own, or is a near-tie: the pre-activation of a flipped ReLU is within
    `TIE` x max|x| of 0, the oracle's max of a flipped window beats the GPU's
    choice by at most `TIE` x max|x| (fractions and margins are reported).
+   TIE = 1e-3 is ten times the forward drift the arithmetic bound below admits
+   (after k steps the GPU's fp32 weights and the oracle's fp64 weights differ by
+   up to ~1e-4 of max|w|, measured r02); a wrong mask or argmax anywhere in the
+   step would show margins of O(1).
 2. Arithmetic: the fp64 oracle evaluated ON THE GPU'S DECISIONS (these hooks:
    ReLU / GradReLU take the GPU mask, MaxPool / GradMaxPool the GPU argmax)
    must match loss, weights and updates to 1e-4 on the reference metric.
@@ -25,7 +29,7 @@ import numpy as np
 
 from oracle import interp_ref as O
 
-TIE = 1e-4
+TIE = 1e-3
 
 
 def gpu_decisions(prog, graph) -> dict:

@@ -28,12 +28,15 @@ def main():
     torch.backends.cuda.matmul.allow_tf32 = False
     g = torch.Generator(device="cuda").manual_seed(0)
     M = Nn = 512
-    for dist in ("uniform", "normal"):
+    for dist in ("uniform", "uniform tf32-exact", "normal"):
         print(f"== {dist} inputs, M=N={M}")
         for Kk in (256, 1024, 4096, 16384, 65536):
-            if dist == "uniform":
+            if dist.startswith("uniform"):
                 a = torch.rand(M, Kk, device="cuda", generator=g)
                 b = torch.rand(Kk, Nn, device="cuda", generator=g)
+                if "exact" in dist:  # zero the 13 low mantissa bits: every product is exact in tf32
+                    a = (a.view(torch.int32) & ~0x1FFF).view(torch.float32)
+                    b = (b.view(torch.int32) & ~0x1FFF).view(torch.float32)
             else:
                 a = torch.randn(M, Kk, device="cuda", generator=g)
                 b = torch.randn(Kk, Nn, device="cuda", generator=g)
