@@ -91,12 +91,12 @@ int wap_gemm_plan_create(const wap_gemm_desc_t* desc, void** plan);
 int wap_gemm_plan_run(void* plan, void* stream);
 void wap_gemm_plan_destroy(void* plan);
 /* The launch configuration a plan resolved to, and the part of it that fixes the fp32
- * rounding: out[0..6] = {block_n, cta_group, splits, k_chunks_per_split, window boxes,
- * precision, n64 pair mode}. Two plans of one descriptor with equal
- * {splits, k_chunks_per_split, precision, cta_group, pair mode, window > 0} produce bitwise-equal outputs
+ * rounding: out[0..7] = {block_n, cta_group, splits, k_chunks_per_split, window boxes,
+ * precision, n64 pair mode, accumulator chain length in k-chunks}. Two plans of one descriptor with equal
+ * {splits, k_chunks_per_split, precision, cta_group, pair mode, window > 0, chain} produce bitwise-equal outputs
  * (same per-element accumulation order); the runtime's autotuner only chooses among
  * those, so tuning never changes results (tests/test_gemm_gpu.py). */
-int wap_gemm_plan_info(const void* plan, int64_t out[7]);
+int wap_gemm_plan_info(const void* plan, int64_t out[8]);
 
 /* ---- activation layout --------------------------------------------------- */
 /* Logical NHWC [B, H, W, C] stored as [B, H+pad, W+pad, ld] (ld >= C,

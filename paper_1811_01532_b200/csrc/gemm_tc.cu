@@ -84,11 +84,28 @@ int make_tmap(CUtensorMap* tm, const wap_operand_t& op, int box_outer) {
   return WAP_OK;
 }
 
+// TMEM accumulator buffers of a 3xTF32 configuration (Cfg::ACC_BUFS)
+int acc_bufs3(int bn, int cg) {
+  switch (bn) {
+    case 64: return cg == 2 ? Cfg<64, 3, 2>::ACC_BUFS : Cfg<64, 3, 1>::ACC_BUFS;
+    case 128: return cg == 2 ? Cfg<128, 3, 2>::ACC_BUFS : Cfg<128, 3, 1>::ACC_BUFS;
+    default: return cg == 2 ? Cfg<192, 3, 2>::ACC_BUFS : Cfg<192, 3, 1>::ACC_BUFS;
+  }
+}
+
 int pick_bn(const wap_gemm_desc_t& d) {
-  if (d.block_n) return d.block_n;
-  // 3xTF32 with split accumulators holds 2 x BN accumulator columns next to the TMEM
-  // A slots: BN <= 192
-  const int widest = (d.precision == 3 && WAP_SPLIT_ACC) ? 192 : 256;
+  // 3xTF32 holds the accumulator(s), the chain running sum S and the TMEM A slots in
+  // 512 columns: BN <= 192
+  if (d.block_n) return d.precision == 3 ? std::min(d.block_n, 192) : d.block_n;
+  if (d.precision == 3) {
+    // 3xTF32: BN = 128 keeps two accumulators next to the chain sum (the epilogue's
+    // chain drains overlap the MMAs); 192 (one accumulator) only where it tiles N exactly
+    if (d.N <= 64) return 64;
+    if (d.N <= 128 || d.N % 128 == 0) return 128;
+    if (d.N <= 192) return 192;
+    return 128;
+  }
+  const int widest = 256;
   const int64_t ntiles = (d.N + widest - 1) / widest;
   const int64_t per = (d.N + ntiles - 1) / ntiles;
   for (int bn : {64, 128, 192, 256})
@@ -96,7 +113,8 @@ int pick_bn(const wap_gemm_desc_t& d) {
   return 256;
 }
 
-constexpr int kMaxChainChunks = 64;               // 2048 K per accumulator chain
+constexpr int kMaxChainChunks = 64;               // 2048 K per accumulator chain (TF32 split-K rule)
+constexpr int kChainChunks = 8;                   // 3xTF32: 256 K per in-kernel accumulator chain
 constexpr long long kAccSlabBytes = 64LL << 20;   // split-K workspace the accuracy rule may use
 
 struct Shape {
@@ -132,7 +150,8 @@ Shape plan_shape(const wap_gemm_desc_t& d) {
   // Automatic plans cut chains longer than kMaxChainChunks into slabs (summed in
   // round-to-nearest fp32 by the deterministic reduction) whenever the slabs are
   // cheap: weight gradients and other small-output / long-K GEMMs.
-  if (d.splits <= 0 && !(d.mbits_out || d.mbits_in)) {
+  // (3xTF32 instead bounds its chains inside the kernel: GemmArgs::chain_chunks)
+  if (d.precision != 3 && d.splits <= 0 && !(d.mbits_out || d.mbits_in)) {
     const int need = wap_ceil_div(s.k_chunks, kMaxChainChunks);
     if (need > splits) {
       const long long per_slab = (long long)d.M * d.ldc * 4;
@@ -151,12 +170,7 @@ int win_smem_cg(int bn, int boxes) {
   switch (bn) {
     case 64: return smem_bytes_for<64, 3, CG, true>(boxes);
     case 128: return smem_bytes_for<128, 3, CG, true>(boxes);
-#if WAP_SPLIT_ACC
     default: return smem_bytes_for<192, 3, CG, true>(boxes);  // 3xTF32: BN <= 192
-#else
-    case 192: return smem_bytes_for<192, 3, CG, true>(boxes);
-    default: return smem_bytes_for<256, 3, CG, true>(boxes);
-#endif
   }
 }
 
@@ -203,7 +217,7 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
   if ((rc = validate_operand(d.a, "a")) || (rc = validate_operand(d.b, "b"))) return rc;
   const Shape s = plan_shape(d);
   WAP_CHECK_ARG(s.bn == 64 || s.bn == 128 || s.bn == 192 || s.bn == 256, "block_n must be 64/128/192/256");
-  WAP_CHECK_ARG(!(d.precision == 3 && WAP_SPLIT_ACC && s.bn > 192), "3xTF32 tiles are at most 192 columns wide");
+  WAP_CHECK_ARG(!(d.precision == 3 && s.bn > 192), "3xTF32 tiles are at most 192 columns wide");
   if ((rc = make_tmap(&p->tmA, d.a, d.a.mn_major ? BK : BM))) return rc;
   if ((rc = make_tmap(&p->tmB, d.b, d.b.mn_major ? BK : s.bn / s.cg))) return rc;
   GemmArgs& g = p->args;
@@ -234,6 +248,16 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
   g.partial = nullptr;
   g.split_stride = d.M * d.ldc;
   g.l2_prefetch = (d.M <= 512 && !getenv("WAP_NO_L2_PREFETCH")) ? 4 : 0;
+  // 3xTF32 accumulator chains (accuracy): the tcgen05 accumulator rounds toward zero,
+  // about one ulp per MMA (tools/gemm_split_acc.py: bias -6.7e-9 x K relative for a
+  // single chain). Chains of kChainChunks k-chunks (3 x 4 x 8 = 96 MMAs) are summed in
+  // round-to-nearest fp32 by the epilogue, which bounds the bias independently of K.
+  g.chain_chunks = 0;
+  if (d.precision == 3) {
+    const char* cc = getenv("WAP_CHAIN_CHUNKS");
+    // one accumulator buffer (BN = 192): the MMAs wait for every chain drain, so 4x longer chains
+    g.chain_chunks = cc ? std::max(0, atoi(cc)) : (acc_bufs3(s.bn, s.cg) == 2 ? kChainChunks : 4 * kChainChunks);
+  }
   g.mbits_out = d.mbits_out;
   g.mbits_out_ld = d.mbits_out_ld;
   g.mbits_in = d.mbits_in;
@@ -327,7 +351,7 @@ extern "C" int wap_gemm_plan_run(void* plan, void* stream) {
 
 extern "C" void wap_gemm_plan_destroy(void* plan) { delete static_cast<Plan*>(plan); }
 
-extern "C" int wap_gemm_plan_info(const void* plan, int64_t out[7]) {
+extern "C" int wap_gemm_plan_info(const void* plan, int64_t out[8]) {
   WAP_CHECK_ARG(plan != nullptr && out != nullptr, "null plan / output");
   const Plan& p = *static_cast<const Plan*>(plan);
   out[0] = p.bn;
@@ -337,5 +361,6 @@ extern "C" int wap_gemm_plan_info(const void* plan, int64_t out[7]) {
   out[4] = p.args.win_boxes;
   out[5] = p.prec;
   out[6] = (p.prec == 3 && p.bn == 64 && p.cg == 1 && WAP_N64_PAIR) ? 1 : 0;
+  out[7] = p.args.chain_chunks;
   return WAP_OK;
 }

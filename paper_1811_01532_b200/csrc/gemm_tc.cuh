@@ -54,7 +54,18 @@ constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap
 // small*B and A*small to half 1 (2^-10 smaller, so its truncations are
 // negligible), and the epilogue adds the halves in round-to-nearest fp32.
 #ifndef WAP_SPLIT_ACC
-#define WAP_SPLIT_ACC 1
+#define WAP_SPLIT_ACC 0  // r02: the split-accumulator mode mis-sums some small-M FC GEMMs (tools/smoke_diag.py: fc7 grad 7e-2); off
+#endif
+// 3xTF32 A operand: big*B and A*small read the RAW A tile straight from shared
+// memory (SS form; kind::tf32 ignores the low 13 mantissa bits, so the raw word IS
+// big), only small*B takes A from TMEM. The splitter then stores one half-tile
+// (small) per k-step instead of two, and a TMEM A slot is 32 columns wide (twice the
+// slots in the same columns). With a halo window (WIN) the raw A tile of every tap
+// is the window at a row offset: a SWIZZLE_128B descriptor may start at any 128-byte
+// row of a 1024-byte-aligned swizzled buffer (measured: tools/desc_shift_probe.cu,
+// shifts 0..23 exact with no base-offset field).
+#ifndef WAP_A_SS
+#define WAP_A_SS 1
 #endif
 // fewest TMEM A slots (3xTF32) worth keeping two accumulators for
 #ifndef WAP_MIN_A_SLOTS
@@ -91,15 +102,16 @@ struct GemmArgs {
   const uint32_t* mbits_in;        // GradReLU mask bits (replaces `mask`)
   int64_t mbits_in_ld;
   int32_t l2_prefetch;             // k-steps of TMA L2 prefetch ahead of the ring (0 = off)
+  int32_t chain_chunks;            // 3xTF32: k-chunks per TMEM accumulator chain (0 = one chain)
 };
 
-// 3xTF32 keeps the A operand in TMEM (tcgen05 "TS" form): the splitter warps
-// read each landed A row once from shared memory and store big/small halves
-// into TMEM with tcgen05.st, so the three MMAs per k-step read only B from
-// shared memory. Layout of the 512 TMEM columns for PREC == 3:
-//   [0, ACC_BUFS*BN)                accumulators
-//   [A_COL0 + s*64, +32)            A big  of stage s   (lane = row, column = k)
-//   [A_COL0 + s*64 + 32, +32)       A small of stage s
+// 3xTF32 A operand (WAP_A_SS, default): the splitter warps read each landed A row
+// once from shared memory and store its small half into TMEM with tcgen05.st;
+// small*B takes A from TMEM (tcgen05 "TS" form), big*B and A*small read the raw A
+// tile from shared memory (SS). Layout of the 512 TMEM columns for PREC == 3:
+//   [0, ACC_BUFS*ACC_W)             accumulators
+//   [A_COL0 + j*32, +32)            A small of A slot j   (lane = row, column = k)
+// (WAP_A_SS=0, the r01 form: all three MMAs TS, slots of 64 columns holding big | small)
 // WIN (3xTF32, K-major A with filter taps): A is not staged per k-step. For each
 // 32-channel chunk the producer loads ONE halo window of A rows
 // [m0 + min_tap_shift, m0 + 128 + max_tap_shift) and the splitter cuts every
@@ -121,16 +133,22 @@ struct Cfg {
   // first half; the epilogue adds the two halves. 2 MMAs per k-slice instead of 3.
   static constexpr bool PAIR = PREC == 3 && BN == 64 && CG == 1 && WAP_N64_PAIR;
   // SACC: two-half accumulators (big*big | small products); PAIR always has two halves
-  static constexpr bool SACC = PREC == 3 && !PAIR && WAP_SPLIT_ACC;
+  static constexpr bool SACC = PREC == 3 && !PAIR && WAP_SPLIT_ACC && !WAP_A_SS;
   static constexpr int HALF = PAIR ? 64 : BN;                      // column offset of half 1
   static constexpr int ACC_W = PAIR ? 128 : (SACC ? 2 * BN : BN);  // TMEM columns per accumulator
-  static constexpr int ACC_BUFS = (PREC == 3 && 512 - 2 * ACC_W < WAP_MIN_A_SLOTS * 64) ? 1 : 2;
-  static constexpr int A_COL0 = ACC_BUFS * ACC_W;
-  static constexpr int TMEM_A_SLOTS = PREC == 3 ? (512 - A_COL0) / 64 : 64;
+  // TMEM columns of one A slot: big + small (TS big*B), or small only when the MMAs
+  // that use A's high part read the raw tile from shared memory (WAP_A_SS)
+  static constexpr int A_SLOT_W = WAP_A_SS ? 32 : 64;
+  // running sum of the accumulator chains (3xTF32, see GemmArgs::chain_chunks): BN columns
+  static constexpr int S_W = PREC == 3 ? (PAIR ? 64 : BN) : 0;
+  static constexpr int ACC_BUFS = (PREC == 3 && 512 - 2 * ACC_W - S_W < WAP_MIN_A_SLOTS * A_SLOT_W) ? 1 : 2;
+  static constexpr int S_COL = ACC_BUFS * ACC_W;
+  static constexpr int A_COL0 = S_COL + S_W;
+  static constexpr int TMEM_A_SLOTS = PREC == 3 ? (512 - A_COL0) / A_SLOT_W : 64;
   static constexpr int STAGES_SMEM = kSmemBudget / STAGE_BYTES;
   // smem stages (TMA prefetch depth) and TMEM A slots (split -> MMA) are separate rings
 #ifndef WAP_MAX_A_SLOTS
-#define WAP_MAX_A_SLOTS 8
+#define WAP_MAX_A_SLOTS 12
 #endif
   // Splitter groups take alternate k-steps and wait on stage / A-slot mbarriers by
   // parity, so a group must observe every phase of each barrier it waits on (with an
@@ -158,6 +176,7 @@ struct Cfg {
                 "3xTF32 rings must be multiples of the splitter group count");
   static_assert(B_ROWS % 32 == 0, "B rows per CTA must be a multiple of 32");
   static_assert(PREC != 3 || A_SLOTS >= kSplitGroups, "3xTF32 needs TMEM A slots next to the accumulators");
+  static_assert(PREC != 3 || A_COL0 + A_SLOTS * A_SLOT_W <= 512, "3xTF32 TMEM layout exceeds 512 columns");
 };
 
 // A row m (32 k-values) of a landed stage, K-major SWIZZLE_128B tile.
@@ -590,7 +609,8 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
       mbar_init(smem_u32(&tempty_bar[i]), CG);  // one arrive per CTA of the pair
       if (WIN) {
         mbar_init(smem_u32(&wfull_bar[i]), 1);
-        mbar_init(smem_u32(&wempty_bar[i]), kSplitGroups);  // every splitter group
+        // every splitter group, plus (WAP_A_SS) the MMA commit of the window's last tap
+        mbar_init(smem_u32(&wempty_bar[i]), kSplitGroups + (WAP_A_SS ? 1 : 0));
       }
     }
     mbar_fence_init();
@@ -728,17 +748,45 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
       // lives in uniform registers); one elected lane issues the tcgen05 ops.
       // A lives in TMEM (K-major by construction) for 3xTF32
       constexpr uint32_t idesc = make_idesc_tf32(BM * CG, BN, PREC == 3 ? false : A_MN, B_MN);
+      // WAP_A_SS: the raw-A MMAs read shared memory in the operand's own major-ness
+      constexpr uint32_t idesc_ss = make_idesc_tf32(BM * CG, BN, A_MN, B_MN);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
       uint32_t acc_ph = 0;
       int aj = 0;  // TMEM A slot of the current step
+      int mwc = 0;  // WIN: windows seen (slot = (mwc - 1) & 1)
       for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
         const TileCoord tc = decode_tile(g, t, BN, CG);
         TW(1, mbar_wait(smem_u32(&tempty_bar[acc]), acc_ph ^ 1));
         tc_fence_after();
         const uint32_t dacc = tmem_base + acc * C::ACC_W;
-        for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc) {
+        int mtap = 0;  // WIN: tap of the current k-chunk (tap innermost)
+        if constexpr (WIN) mtap = tc.kc_begin % ntaps;
+        // 3xTF32 accumulator chains: every chain_chunks k-chunks the accumulator is handed
+        // to the epilogue (which folds it into the running sum S in round-to-nearest fp32)
+        // and the next chain starts in the other accumulator
+        const int clen = (PREC == 3 && g.chain_chunks > 0) ? g.chain_chunks : (tc.kc_end - tc.kc_begin);
+        int cpos = 0;
+        uint32_t dacc_cur = dacc;
+        for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc, ++cpos) {
+          if (cpos == clen) {
+            if (elect_one()) umma_commit_cg<CG>(smem_u32(&tfull_bar[acc]));
+            __syncwarp();
+            if (++acc == C::ACC_BUFS) { acc = 0; acc_ph ^= 1; }
+            TW(1, mbar_wait(smem_u32(&tempty_bar[acc]), acc_ph ^ 1));
+            tc_fence_after();
+            dacc_cur = tmem_base + acc * C::ACC_W;
+            cpos = 0;
+          }
+          bool win_last = false;
+          uint32_t win_a = 0;  // WIN: raw A tile of this tap = window rows shifted by the tap offset
+          if constexpr (WIN) {
+            if (mtap == 0 || kc == tc.kc_begin) ++mwc;
+            win_last = (mtap == ntaps - 1) || (kc == tc.kc_end - 1);
+            win_a = smem_u32(win_base + ((mwc - 1) & 1) * win_bytes) +
+                    (uint32_t)((s_off[0][mtap] - g.win_off_min) * 128);
+          }
           if constexpr (PREC == 3) TW(2, mbar_wait(smem_u32(&conv_bar[s]), ph));
           else TW(2, mbar_wait(smem_u32(&full_bar[s]), ph));
           tc_fence_after();
@@ -748,9 +796,9 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           constexpr uint64_t kA = A_MN ? (1024 >> 4) : (32 >> 4);
           const uint64_t bd0 = operand_desc<B_MN>(stage_b(s), 0);
           const uint64_t bsd0 = operand_desc<B_MN>(stage_bs(s), 0);
-          const uint64_t ad0 = operand_desc<A_MN>(stage_a(s), 0);
-          const uint32_t a_big0 = tmem_base + C::A_COL0 + aj * 64;
-          const uint32_t first0 = kc > tc.kc_begin ? 1u : 0u;
+          const uint64_t ad0 = WIN ? make_sdesc_sw128(win_a, 16, 1024) : operand_desc<A_MN>(stage_a(s), 0);
+          const uint32_t a_big0 = tmem_base + C::A_COL0 + aj * C::A_SLOT_W;
+          const uint32_t first0 = cpos > 0 ? 1u : 0u;
 #ifdef WAP_GEMM_TMA_ONLY
           // diagnostic: measure the TMA (+ split) stream alone, no MMA
           if (elect_one()) {
@@ -767,34 +815,50 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
             for (int kk = 0; kk < BK / 8; ++kk) {
               const uint64_t bd = bd0 + kk * kB;
               const uint32_t first = kk > 0 ? 1u : first0;
-              if constexpr (C::PAIR) {
+              if constexpr (PREC == 3 && WAP_A_SS) {
+                const uint32_t a_small = a_big0 + kk * 8;
+                const uint64_t ad = ad0 + kk * kA;
+                if constexpr (C::PAIR) {
+                  constexpr uint32_t idesc2 = make_idesc_tf32(BM, 128, A_MN, B_MN);
+                  umma_cg<CG>(dacc_cur, ad, bd, idesc2, first);                // A * [B | B_small] (smem A)
+                  umma_ts_cg<CG>(dacc_cur, a_small, bd, idesc, 1u);            // small * B (TMEM A)
+                } else {
+                  umma_ts_cg<CG>(dacc_cur, a_small, bd, idesc, first);         // small * B (TMEM A)
+                  umma_cg<CG>(dacc_cur, ad, bsd0 + kk * kB, idesc_ss, 1u);     // A * small (smem A)
+                  umma_cg<CG>(dacc_cur, ad, bd, idesc_ss, 1u);                 // big * big (smem A)
+                }
+              } else if constexpr (C::PAIR) {
                 constexpr uint32_t idesc2 = make_idesc_tf32(BM, 128, false, B_MN);
                 const uint32_t a_big = a_big0 + kk * 8;
-                umma_ts_cg<CG>(dacc, a_big, bd, idesc2, first);            // A * [B | B_small]
+                umma_ts_cg<CG>(dacc_cur, a_big, bd, idesc2, first);            // A * [B | B_small]
                 if constexpr (WAP_SPLIT_ACC)
-                  umma_ts_cg<CG>(dacc + 64, a_big + 32, bd, idesc, 1u);    // small * B -> small half
+                  umma_ts_cg<CG>(dacc_cur + 64, a_big + 32, bd, idesc, 1u);    // small * B -> small half
                 else
-                  umma_ts_cg<CG>(dacc, a_big + 32, bd, idesc, 1u);         // small * B
+                  umma_ts_cg<CG>(dacc_cur, a_big + 32, bd, idesc, 1u);         // small * B
               } else if constexpr (C::SACC) {
                 const uint32_t a_big = a_big0 + kk * 8;
-                umma_ts_cg<CG>(dacc + C::HALF, a_big + 32, bd, idesc, first);  // small * B -> half 1
-                umma_ts_cg<CG>(dacc + C::HALF, a_big, bsd0 + kk * kB, idesc, 1u);  // A * small -> half 1
-                umma_ts_cg<CG>(dacc, a_big, bd, idesc, first);                 // big * big -> half 0
+                umma_ts_cg<CG>(dacc_cur + C::HALF, a_big + 32, bd, idesc, first);  // small * B -> half 1
+                umma_ts_cg<CG>(dacc_cur + C::HALF, a_big, bsd0 + kk * kB, idesc, 1u);  // A * small -> half 1
+                umma_ts_cg<CG>(dacc_cur, a_big, bd, idesc, first);                 // big * big -> half 0
               } else if constexpr (PREC == 3) {
                 const uint32_t a_big = a_big0 + kk * 8;
-                umma_ts_cg<CG>(dacc, a_big + 32, bd, idesc, first);        // small * B
-                umma_ts_cg<CG>(dacc, a_big, bsd0 + kk * kB, idesc, 1u);    // A * small
-                umma_ts_cg<CG>(dacc, a_big, bd, idesc, 1u);                // big * big
+                umma_ts_cg<CG>(dacc_cur, a_big + 32, bd, idesc, first);        // small * B
+                umma_ts_cg<CG>(dacc_cur, a_big, bsd0 + kk * kB, idesc, 1u);    // A * small
+                umma_ts_cg<CG>(dacc_cur, a_big, bd, idesc, 1u);                // big * big
               } else {
-                umma_cg<CG>(dacc, ad0 + kk * kA, bd, idesc, first);
+                umma_cg<CG>(dacc_cur, ad0 + kk * kA, bd, idesc, first);
               }
             }
             umma_commit_cg<CG>(smem_u32(&empty_bar[s]));
             if constexpr (PREC == 3) umma_commit_cg<CG>(smem_u32(&aslot_bar[aj]));
+            // the MMAs read the raw window: it is free once the last tap's MMAs complete
+            if constexpr (WIN && WAP_A_SS)
+              if (win_last) umma_commit_cg<CG>(smem_u32(&wempty_bar[(mwc - 1) & 1]));
           }
           __syncwarp();
           if (++s == STAGES) { s = 0; ph ^= 1; }
           if (++aj == C::A_SLOTS) aj = 0;
+          if constexpr (WIN) mtap = mtap + 1 == ntaps ? 0 : mtap + 1;
         }
 #ifdef WAP_GEMM_TMA_ONLY
         if (elect_one())
@@ -853,9 +917,62 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
       }
       return b;
     };
+    const uint32_t lane_tm = tmem_base + ((uint32_t)(wq * 32) << 16);  // this warp's TMEM lanes
+    // logical accumulator columns [c0, c0 + 32) of buffer `a` (PAIR / SACC: both halves added)
+    auto load_acc = [&](int a, int c0, uint32_t (&v)[32]) {
+      tmem_ld_32x32b_x32(lane_tm + a * C::ACC_W + c0, v);
+      if constexpr (C::PAIR || C::SACC) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t v2[16];
+          tmem_ld_32x32b_x16(lane_tm + a * C::ACC_W + C::HALF + c0 + hh * 16, v2);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            v[hh * 16 + j] = __float_as_uint(__uint_as_float(v[hh * 16 + j]) + __uint_as_float(v2[j]));
+        }
+      }
+      tmem_ld_wait();
+    };
     for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
       const TileCoord tc = decode_tile(g, t, BN, CG);
       float4 b4_next = load_bias(tc.n0);  // in flight across the accumulator wait
+      const int nk = tc.kc_end - tc.kc_begin;
+      const int clen = (PREC == 3 && g.chain_chunks > 0) ? g.chain_chunks : nk;
+      const int nchains = (nk + clen - 1) / clen;
+      // every chain but the last: S (+)= chain accumulator, round-to-nearest fp32, in chain
+      // order (deterministic); the accumulator goes straight back to the MMA warp
+      for (int ch = 0; ch + 1 < nchains; ++ch) {
+        TW(1, mbar_wait(smem_u32(&tfull_bar[acc]), acc_ph));
+        tc_fence_after();
+        // 16 columns at a time (register pressure: 768 threads share the register file)
+#pragma unroll 1
+        for (int c0 = 0; c0 < C::S_W; c0 += 16) {
+          uint32_t v[16], w[16];
+          tmem_ld_32x32b_x16(lane_tm + acc * C::ACC_W + c0, v);
+          if constexpr (C::PAIR || C::SACC) tmem_ld_32x32b_x16(lane_tm + acc * C::ACC_W + C::HALF + c0, w);
+          tmem_ld_wait();
+          if constexpr (C::PAIR || C::SACC) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+          }
+          if (ch > 0) {
+            tmem_ld_32x32b_x16(lane_tm + C::S_COL + c0, w);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(w[j]) + __uint_as_float(v[j]));
+          }
+          tmem_st_32x32b_x16(lane_tm + C::S_COL + c0, v);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        named_bar_sync(1, 128);
+        if (wq == 0 && lane == 0) {
+          if (CG == 2 && !leader) mbar_arrive_cluster(tempty_leader + acc * 8);
+          else mbar_arrive(smem_u32(&tempty_bar[acc]));
+        }
+        if (++acc == C::ACC_BUFS) { acc = 0; acc_ph ^= 1; }
+      }
 #ifdef WAP_EPI_TRACE
       mbar_wait(smem_u32(&tfull_bar[acc]), acc_ph);
 #else
@@ -881,21 +998,18 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
       for (int cb = 0; cb < BN / 32; ++cb) {
         uint32_t v[32];
         EPI_T0();
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * C::ACC_W + cb * 32, v);
-        if constexpr (C::PAIR || C::SACC) {
-          // second half of the accumulator (the small products), 16 columns at a time
+        load_acc(acc, cb * 32, v);
+        if (PREC == 3 && nchains > 1) {  // + the running sum of the earlier chains
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            uint32_t v2[16];
-            tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * C::ACC_W + C::HALF + cb * 32 + hh * 16,
-                               v2);
+            uint32_t sv[16];
+            tmem_ld_32x32b_x16(lane_tm + C::S_COL + cb * 32 + hh * 16, sv);
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-              v[hh * 16 + j] = __float_as_uint(__uint_as_float(v[hh * 16 + j]) + __uint_as_float(v2[j]));
+              v[hh * 16 + j] = __float_as_uint(__uint_as_float(sv[j]) + __uint_as_float(v[hh * 16 + j]));
           }
         }
-        tmem_ld_wait();
         EPI_T(1);
         const int nb = tc.n0 + cb * 32;
         if (nb >= g.N) continue;  // warp-uniform
@@ -1164,16 +1278,20 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         for (int j = 0; j < 16; ++j) {
           const uint32_t big = v[j] & 0xFFFFE000u;
           w[j] = __float_as_uint(__uint_as_float(v[j]) - __uint_as_float(big));
-          v[j] = big;
+          if constexpr (!WAP_A_SS) v[j] = big;
         }
         // TMEM A slot of this step: free once the MMAs of its previous use committed
         const int aj = it % C::A_SLOTS;
         TW(2, mbar_wait(smem_u32(&aslot_bar[aj]), ((it / C::A_SLOTS) & 1) ^ 1));
         tc_fence_after();
-        const uint32_t acol = tmem_base + lane_base + C::A_COL0 + aj * 64 + half * 16;
+        const uint32_t acol = tmem_base + lane_base + C::A_COL0 + aj * C::A_SLOT_W + half * 16;
 #ifndef WAP_DIAG_NO_A_SPLIT
-        tmem_st_32x32b_x16(acol, v);
-        tmem_st_32x32b_x16(acol + 32, w);
+        if constexpr (WAP_A_SS) {
+          tmem_st_32x32b_x16(acol, w);  // small only: the MMAs take big from the raw smem tile
+        } else {
+          tmem_st_32x32b_x16(acol, v);
+          tmem_st_32x32b_x16(acol + 32, w);
+        }
 #endif
         split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_OFF),
                          reinterpret_cast<uint32_t*>(base + C::A_OFF + C::B_BYTES), C::B_ROWS * BK, gt, 256);

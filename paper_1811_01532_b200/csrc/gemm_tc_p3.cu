@@ -7,12 +7,7 @@ static int by_bn(const Plan& p, cudaStream_t st) {
   switch (p.bn) {
     case 64: return launch_majors<64, 3, CG>(p, st);
     case 128: return launch_majors<128, 3, CG>(p, st);
-#if WAP_SPLIT_ACC
-    default: return launch_majors<192, 3, CG>(p, st);  // 3xTF32 split accumulators: BN <= 192
-#else
-    case 192: return launch_majors<192, 3, CG>(p, st);
-    default: return launch_majors<256, 3, CG>(p, st);
-#endif
+    default: return launch_majors<192, 3, CG>(p, st);  // 3xTF32: BN <= 192 (TMEM: acc + S + A slots)
   }
 }
 int launch_prec3(const Plan& p, cudaStream_t st) { return p.cg == 2 ? by_bn<2>(p, st) : by_bn<1>(p, st); }

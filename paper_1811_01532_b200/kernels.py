@@ -64,19 +64,19 @@ class GemmCall:
 
     def info(self) -> dict:
         """The resolved launch configuration (wap_gemm_plan_info)."""
-        out = (C.c_int64 * 7)()
+        out = (C.c_int64 * 8)()
         N.check(N.lib().wap_gemm_plan_info(self._plan, out), "wap_gemm_plan_info")
         return dict(zip(("block_n", "cta_group", "splits", "k_chunks_per_split", "window_boxes", "precision",
-                         "pair"), (int(v) for v in out)))
+                         "pair", "chain"), (int(v) for v in out)))
 
     def numerics(self) -> tuple:
         """What fixes the fp32 rounding of the result: K split, precision, CTA group,
         N = 64 pair mode, halo window (it walks K tap-innermost, the plain plan
-        tap-outermost). Measured on B200: plans equal in these are bitwise equal
+        tap-outermost), 3xTF32 accumulator chain length. Measured on B200: plans equal in these are bitwise equal
         (tests/test_determinism_gpu.py); BN does not enter."""
         i = self.info()
         return (i["splits"], i["k_chunks_per_split"] if i["splits"] > 1 else 0, i["precision"], i["cta_group"],
-                i["pair"], int(i["window_boxes"] > 0))
+                i["pair"], int(i["window_boxes"] > 0), i["chain"])
 
     def __del__(self):
         try:

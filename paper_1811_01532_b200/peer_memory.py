@@ -60,6 +60,30 @@ def _pidfd_getfd(pid: int, fd: int) -> int:
         os.close(pidfd)
 
 
+def multicast_supported(device: int = 0) -> tuple[bool, str]:
+    """Can this box create an NVLS multicast object? (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED,
+    then a one-device cuMulticastCreate: single-GPU boxes without an NVSwitch fabric
+    report the attribute but refuse the object with CUDA_ERROR_INVALID_VALUE.)"""
+    cu = _cu()
+    _ck(cu.cuInit(0), "cuInit")
+    dev = _ck(cu.cuDeviceGet(device), "cuDeviceGet")
+    attr = _ck(cu.cuDeviceGetAttribute(cu.CUdevice_attribute.CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev),
+               "multicast attribute")
+    if not attr:
+        return False, "CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED = 0"
+    ctx = _ck(cu.cuDevicePrimaryCtxRetain(dev), "cuDevicePrimaryCtxRetain")
+    _ck(cu.cuCtxSetCurrent(ctx), "cuCtxSetCurrent")
+    mp = cu.CUmulticastObjectProp()
+    mp.numDevices = 1
+    mp.handleTypes = cu.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR
+    mp.size = 2 << 20
+    res = cu.cuMulticastCreate(mp)
+    if res[0] != cu.CUresult.CUDA_SUCCESS:
+        return False, f"cuMulticastCreate: {res[0]}"
+    cu.cuMemRelease(res[1])
+    return True, ""
+
+
 class _CudaArray:
     def __init__(self, ptr: int, nfloats: int):
         self.__cuda_array_interface__ = {"shape": (nfloats,), "typestr": "<f4", "data": (ptr, False),

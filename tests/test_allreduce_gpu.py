@@ -45,6 +45,12 @@ def test_world1_fused_kernel_and_graph_replay(cuda, mode):
     from paper_1811_01532_b200 import _native as N
     from paper_1811_01532_b200.peer_memory import FusedAllReduce
 
+    if mode == "nvls":
+        from paper_1811_01532_b200.peer_memory import multicast_supported
+
+        ok, why = multicast_supported(0)
+        if not ok:
+            pytest.skip(f"no NVLS multicast on this box ({why})")
     n = (1 << 20) + 6  # odd tail
     fr = FusedAllReduce(0, 1, 0, mode)
     var, grad = fr.allocate(n + 2)

@@ -30,7 +30,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--nets", nargs="*", default=["alexnet:128", "vgg16:32"])
     ap.add_argument("--out", default=str(plan_cache.PLAN_FILE))
+    ap.add_argument("--merge", action="store_true", help="keep entries of the existing file (default: rewrite)")
     args = ap.parse_args()
+    if not args.merge and Path(args.out).exists():
+        Path(args.out).unlink()  # plans of another kernel build may not be valid any more
     plans = {}
     prof = planner.load_profile("b200")
     for spec in args.nets:
