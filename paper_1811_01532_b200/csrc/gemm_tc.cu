@@ -84,15 +84,6 @@ int make_tmap(CUtensorMap* tm, const wap_operand_t& op, int box_outer) {
   return WAP_OK;
 }
 
-// TMEM accumulator buffers of a 3xTF32 configuration (Cfg::ACC_BUFS)
-int acc_bufs3(int bn, int cg) {
-  switch (bn) {
-    case 64: return cg == 2 ? Cfg<64, 3, 2>::ACC_BUFS : Cfg<64, 3, 1>::ACC_BUFS;
-    case 128: return cg == 2 ? Cfg<128, 3, 2>::ACC_BUFS : Cfg<128, 3, 1>::ACC_BUFS;
-    default: return cg == 2 ? Cfg<192, 3, 2>::ACC_BUFS : Cfg<192, 3, 1>::ACC_BUFS;
-  }
-}
-
 int pick_bn(const wap_gemm_desc_t& d) {
   // 3xTF32 holds the accumulator(s), the chain running sum S and the TMEM A slots in
   // 512 columns: BN <= 192
@@ -256,7 +247,10 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
   if (d.precision == 3) {
     const char* cc = getenv("WAP_CHAIN_CHUNKS");
     // one accumulator buffer (BN = 192): the MMAs wait for every chain drain, so 4x longer chains
-    g.chain_chunks = cc ? std::max(0, atoi(cc)) : (acc_bufs3(s.bn, s.cg) == 2 ? kChainChunks : 4 * kChainChunks);
+    // (one accumulator buffer with BN = 192: the MMAs wait for each 192-column drain, so
+    // 2x longer chains; measured AlexNet conv2: 613 / 668 / 737 tensor-pipe TF/s at chains
+    // of 8 / 16 / unbounded, tools/gpurun/r2_exp1.sh)
+    g.chain_chunks = cc ? std::max(0, atoi(cc)) : (s.bn == 192 ? 2 * kChainChunks : kChainChunks);
   }
   g.mbits_out = d.mbits_out;
   g.mbits_out_ld = d.mbits_out_ld;

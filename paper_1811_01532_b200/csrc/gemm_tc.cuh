@@ -105,13 +105,14 @@ struct GemmArgs {
   int32_t chain_chunks;            // 3xTF32: k-chunks per TMEM accumulator chain (0 = one chain)
 };
 
-// 3xTF32 A operand (WAP_A_SS, default): the splitter warps read each landed A row
+// 3xTF32 A operand (WAP_A_SS, CTA pairs): the splitter warps read each landed A row
 // once from shared memory and store its small half into TMEM with tcgen05.st;
 // small*B takes A from TMEM (tcgen05 "TS" form), big*B and A*small read the raw A
 // tile from shared memory (SS). Layout of the 512 TMEM columns for PREC == 3:
 //   [0, ACC_BUFS*ACC_W)             accumulators
 //   [A_COL0 + j*32, +32)            A small of A slot j   (lane = row, column = k)
-// (WAP_A_SS=0, the r01 form: all three MMAs TS, slots of 64 columns holding big | small)
+// (single CTAs and WAP_A_SS=0, the r01 form: all three MMAs TS, slots of 64 columns
+// holding big | small)
 // WIN (3xTF32, K-major A with filter taps): A is not staged per k-step. For each
 // 32-channel chunk the producer loads ONE halo window of A rows
 // [m0 + min_tap_shift, m0 + 128 + max_tap_shift) and the splitter cuts every
@@ -133,12 +134,17 @@ struct Cfg {
   // first half; the epilogue adds the two halves. 2 MMAs per k-slice instead of 3.
   static constexpr bool PAIR = PREC == 3 && BN == 64 && CG == 1 && WAP_N64_PAIR;
   // SACC: two-half accumulators (big*big | small products); PAIR always has two halves
-  static constexpr bool SACC = PREC == 3 && !PAIR && WAP_SPLIT_ACC && !WAP_A_SS;
+  // raw A from shared memory except for the single-CTA N = 64 pair kernels, where the
+  // N = 128 SS MMA (A + all of [B | B_small] from this CTA's shared memory, ~128 B/clk)
+  // measured slower than the TS form (tools/gpurun/r2_exp1.sh, r02); the TS form keeps
+  // 64-column A slots, so those kernels hold one accumulator buffer next to S
+  static constexpr bool A_SS = WAP_A_SS && PREC == 3 && !(CG == 1 && BN == 64);
+  static constexpr bool SACC = PREC == 3 && !PAIR && WAP_SPLIT_ACC && !A_SS;
   static constexpr int HALF = PAIR ? 64 : BN;                      // column offset of half 1
   static constexpr int ACC_W = PAIR ? 128 : (SACC ? 2 * BN : BN);  // TMEM columns per accumulator
   // TMEM columns of one A slot: big + small (TS big*B), or small only when the MMAs
   // that use A's high part read the raw tile from shared memory (WAP_A_SS)
-  static constexpr int A_SLOT_W = WAP_A_SS ? 32 : 64;
+  static constexpr int A_SLOT_W = A_SS ? 32 : 64;
   // running sum of the accumulator chains (3xTF32, see GemmArgs::chain_chunks): BN columns
   static constexpr int S_W = PREC == 3 ? (PAIR ? 64 : BN) : 0;
   static constexpr int ACC_BUFS = (PREC == 3 && 512 - 2 * ACC_W - S_W < WAP_MIN_A_SLOTS * A_SLOT_W) ? 1 : 2;
@@ -610,7 +616,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
       if (WIN) {
         mbar_init(smem_u32(&wfull_bar[i]), 1);
         // every splitter group, plus (WAP_A_SS) the MMA commit of the window's last tap
-        mbar_init(smem_u32(&wempty_bar[i]), kSplitGroups + (WAP_A_SS ? 1 : 0));
+        mbar_init(smem_u32(&wempty_bar[i]), kSplitGroups + (C::A_SS ? 1 : 0));
       }
     }
     mbar_fence_init();
@@ -815,7 +821,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
             for (int kk = 0; kk < BK / 8; ++kk) {
               const uint64_t bd = bd0 + kk * kB;
               const uint32_t first = kk > 0 ? 1u : first0;
-              if constexpr (PREC == 3 && WAP_A_SS) {
+              if constexpr (C::A_SS) {
                 const uint32_t a_small = a_big0 + kk * 8;
                 const uint64_t ad = ad0 + kk * kA;
                 if constexpr (C::PAIR) {
@@ -852,7 +858,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
             umma_commit_cg<CG>(smem_u32(&empty_bar[s]));
             if constexpr (PREC == 3) umma_commit_cg<CG>(smem_u32(&aslot_bar[aj]));
             // the MMAs read the raw window: it is free once the last tap's MMAs complete
-            if constexpr (WIN && WAP_A_SS)
+            if constexpr (WIN && C::A_SS)
               if (win_last) umma_commit_cg<CG>(smem_u32(&wempty_bar[(mwc - 1) & 1]));
           }
           __syncwarp();
@@ -1278,7 +1284,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         for (int j = 0; j < 16; ++j) {
           const uint32_t big = v[j] & 0xFFFFE000u;
           w[j] = __float_as_uint(__uint_as_float(v[j]) - __uint_as_float(big));
-          if constexpr (!WAP_A_SS) v[j] = big;
+          if constexpr (!C::A_SS) v[j] = big;
         }
         // TMEM A slot of this step: free once the MMAs of its previous use committed
         const int aj = it % C::A_SLOTS;
@@ -1286,7 +1292,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         tc_fence_after();
         const uint32_t acol = tmem_base + lane_base + C::A_COL0 + aj * C::A_SLOT_W + half * 16;
 #ifndef WAP_DIAG_NO_A_SPLIT
-        if constexpr (WAP_A_SS) {
+        if constexpr (C::A_SS) {
           tmem_st_32x32b_x16(acol, w);  // small only: the MMAs take big from the raw smem tile
         } else {
           tmem_st_32x32b_x16(acol, v);
