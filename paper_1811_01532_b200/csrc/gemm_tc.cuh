@@ -67,6 +67,12 @@ constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap
 #ifndef WAP_A_SS
 #define WAP_A_SS 1
 #endif
+#ifndef WAP_B_SPLIT_EARLY
+#define WAP_B_SPLIT_EARLY 1
+#endif
+#ifndef WAP_WIN_SMALL
+#define WAP_WIN_SMALL 1
+#endif
 // fewest TMEM A slots (3xTF32) worth keeping two accumulators for
 #ifndef WAP_MIN_A_SLOTS
 #define WAP_MIN_A_SLOTS 4
@@ -147,7 +153,14 @@ struct Cfg {
   static constexpr int A_SLOT_W = A_SS ? 32 : 64;
   // running sum of the accumulator chains (3xTF32, see GemmArgs::chain_chunks): BN columns
   static constexpr int S_W = PREC == 3 ? (PAIR ? 64 : BN) : 0;
-  static constexpr int ACC_BUFS = (PREC == 3 && 512 - 2 * ACC_W - S_W < WAP_MIN_A_SLOTS * A_SLOT_W) ? 1 : 2;
+  // WSS (halo window, CTA pair): the small half of the whole A window is computed once
+  // per channel chunk into shared memory next to the raw window, and all three MMAs
+  // of every tap read A from the window (SS): no per-tap A split, no TMEM A slots
+  static constexpr bool WSS = WIN && A_SS && WAP_WIN_SMALL && BN <= 128;
+  static constexpr int WIN_MUL = WSS ? 2 : 1;  // window slot = raw (| small)
+  static constexpr int ACC_BUFS =
+      WSS ? ((2 * ACC_W + S_W <= 512) ? 2 : 1)
+          : ((PREC == 3 && 512 - 2 * ACC_W - S_W < WAP_MIN_A_SLOTS * A_SLOT_W) ? 1 : 2);
   static constexpr int S_COL = ACC_BUFS * ACC_W;
   static constexpr int A_COL0 = S_COL + S_W;
   static constexpr int TMEM_A_SLOTS = PREC == 3 ? (512 - A_COL0) / A_SLOT_W : 64;
@@ -173,7 +186,10 @@ struct Cfg {
   }
   static constexpr int A_SLOTS =
       PREC == 3 ? ring_round(TMEM_A_SLOTS > WAP_MAX_A_SLOTS ? WAP_MAX_A_SLOTS : TMEM_A_SLOTS) : 1;
-  static constexpr int STAGES = WIN ? 6 : ring_round(STAGES_SMEM > 8 ? 8 : STAGES_SMEM);
+  // (WSS: the small window doubles the window footprint; 4 B stages keep one window pair
+  // of 2 boxes + stages + epilogue staging under 227 KB for BN <= 128)
+  static constexpr int STAGES = WIN ? ((WIN && A_SS && WAP_WIN_SMALL && BN <= 128) ? 4 : 6)
+                                    : ring_round(STAGES_SMEM > 8 ? 8 : STAGES_SMEM);
   static constexpr int TMEM_COLS = PREC == 3 ? 512 : ((2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512));
   static constexpr int THREADS = PREC == 3 ? 256 + 256 * kSplitGroups : 256;  // + splitter warp groups
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + kEpiStage + kBarBytes;
@@ -182,7 +198,8 @@ struct Cfg {
                 "3xTF32 rings must be multiples of the splitter group count");
   static_assert(B_ROWS % 32 == 0, "B rows per CTA must be a multiple of 32");
   static_assert(PREC != 3 || A_SLOTS >= kSplitGroups, "3xTF32 needs TMEM A slots next to the accumulators");
-  static_assert(PREC != 3 || A_COL0 + A_SLOTS * A_SLOT_W <= 512, "3xTF32 TMEM layout exceeds 512 columns");
+  static_assert(PREC != 3 || WSS || A_COL0 + A_SLOTS * A_SLOT_W <= 512, "3xTF32 TMEM layout exceeds 512 columns");
+  static_assert(!WSS || kSplitGroups == 2, "WSS assigns window slot g to splitter group g");
 };
 
 // A row m (32 k-values) of a landed stage, K-major SWIZZLE_128B tile.
@@ -570,11 +587,13 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* win_base = smem + STAGES * C::STAGE_BYTES;                  // 2 A halo windows (WIN)
   const int win_bytes = WIN ? g.win_boxes * C::A_BYTES : 0;
-  uint8_t* epi_base = win_base + 2 * win_bytes;                        // 1024-aligned staging
+  const int win_slot = win_bytes * C::WIN_MUL;                          // raw window (| its small half)
+  uint8_t* epi_base = win_base + 2 * win_slot;                         // 1024-aligned staging
   uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + kEpiStage);
   uint64_t* wfull_bar = bars + 3 * STAGES + 5;   // [2] window landed (WIN)
   uint64_t* wempty_bar = bars + 3 * STAGES + 7;  // [2] window consumed by both splitter groups (WIN)
   uint64_t* aslot_bar = bars + 3 * STAGES + 9;   // [A_SLOTS] TMEM A slot free again (MMA commit)
+  uint64_t* wsmall_bar = aslot_bar + C::A_SLOTS;  // [2] WSS: window's small half written (leader-side)
   uint64_t* full_bar = bars;                    // TMA landed (leader-side for CG=2 & TF32)
   uint64_t* empty_bar = bars + STAGES;          // smem slot free (MMA commit, multicast)
   uint64_t* conv_bar = bars + 2 * STAGES;       // 3xTF32 split done (leader-side)
@@ -615,8 +634,10 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
       mbar_init(smem_u32(&tempty_bar[i]), CG);  // one arrive per CTA of the pair
       if (WIN) {
         mbar_init(smem_u32(&wfull_bar[i]), 1);
-        // every splitter group, plus (WAP_A_SS) the MMA commit of the window's last tap
-        mbar_init(smem_u32(&wempty_bar[i]), kSplitGroups + (C::A_SS ? 1 : 0));
+        // every splitter group, plus (WAP_A_SS) the MMA commit of the window's last tap;
+        // WSS: the MMA commit alone (the owning group's window read precedes wsmall)
+        mbar_init(smem_u32(&wempty_bar[i]), C::WSS ? 1 : kSplitGroups + (C::A_SS ? 1 : 0));
+        mbar_init(smem_u32(&wsmall_bar[i]), CG);  // WSS: one arrive per CTA of the pair
       }
     }
     mbar_fence_init();
@@ -670,7 +691,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
               const uint32_t wb = smem_u32(&wfull_bar[ws]);
               mbar_arrive_expect_tx(wb, win_bytes);
               TW(3, for (int bx = 0; bx < g.win_boxes; ++bx)
-                tma_load_2d(smem_u32(win_base + ws * win_bytes + bx * C::A_BYTES), &tmA, wb, w_cidx * BK,
+                tma_load_2d(smem_u32(win_base + ws * win_slot + bx * C::A_BYTES), &tmA, wb, w_cidx * BK,
                             a_row0 + g.win_off_min + bx * BM));
               ++wc;
             }
@@ -788,9 +809,13 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           bool win_last = false;
           uint32_t win_a = 0;  // WIN: raw A tile of this tap = window rows shifted by the tap offset
           if constexpr (WIN) {
-            if (mtap == 0 || kc == tc.kc_begin) ++mwc;
+            if (mtap == 0 || kc == tc.kc_begin) {
+              ++mwc;
+              // WSS: both CTAs' small halves of this window are written
+              if constexpr (C::WSS) TW(2, mbar_wait(smem_u32(&wsmall_bar[(mwc - 1) & 1]), ((mwc - 1) >> 1) & 1));
+            }
             win_last = (mtap == ntaps - 1) || (kc == tc.kc_end - 1);
-            win_a = smem_u32(win_base + ((mwc - 1) & 1) * win_bytes) +
+            win_a = smem_u32(win_base + ((mwc - 1) & 1) * win_slot) +
                     (uint32_t)((s_off[0][mtap] - g.win_off_min) * 128);
           }
           if constexpr (PREC == 3) TW(2, mbar_wait(smem_u32(&conv_bar[s]), ph));
@@ -821,7 +846,14 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
             for (int kk = 0; kk < BK / 8; ++kk) {
               const uint64_t bd = bd0 + kk * kB;
               const uint32_t first = kk > 0 ? 1u : first0;
-              if constexpr (C::A_SS) {
+              if constexpr (C::WSS) {
+                // all SS: small half of the window at win_bytes past the raw window
+                const uint64_t ad = ad0 + kk * kA;
+                const uint64_t as = ad + (uint64_t)(win_bytes >> 4);
+                umma_cg<CG>(dacc_cur, as, bd, idesc_ss, first);                // small * B
+                umma_cg<CG>(dacc_cur, ad, bsd0 + kk * kB, idesc_ss, 1u);       // A * small
+                umma_cg<CG>(dacc_cur, ad, bd, idesc_ss, 1u);                   // big * big
+              } else if constexpr (C::A_SS) {
                 const uint32_t a_small = a_big0 + kk * 8;
                 const uint64_t ad = ad0 + kk * kA;
                 if constexpr (C::PAIR) {
@@ -856,7 +888,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
               }
             }
             umma_commit_cg<CG>(smem_u32(&empty_bar[s]));
-            if constexpr (PREC == 3) umma_commit_cg<CG>(smem_u32(&aslot_bar[aj]));
+            if constexpr (PREC == 3 && !C::WSS) umma_commit_cg<CG>(smem_u32(&aslot_bar[aj]));
             // the MMAs read the raw window: it is free once the last tap's MMAs complete
             if constexpr (WIN && C::A_SS)
               if (win_last) umma_commit_cg<CG>(smem_u32(&wempty_bar[(mwc - 1) & 1]));
@@ -1224,6 +1256,47 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
     int it = 0;
     int wc = 0, wslot = 0;       // WIN: windows seen, current slot
     bool wwaited = false;        // WIN: this group has waited for the current window
+    if constexpr (C::WSS) {
+      // Window slot g belongs to group g: it waits for every landing of its slot (so its
+      // parity waits never skip a phase), writes the small half of the whole window once,
+      // and signals wsmall; per k-step a group only splits its B stage.
+      const uint32_t wsmall_leader = CG == 2 ? map_to_rank(smem_u32(&wsmall_bar[0]), 0) : smem_u32(&wsmall_bar[0]);
+      for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
+        const TileCoord tc = decode_tile(g, t, BN, CG);
+        int tap = tc.kc_begin % ntaps;
+        for (int kc = tc.kc_begin; kc < tc.kc_end; ++kc, ++it, tap = tap + 1 == ntaps ? 0 : tap + 1) {
+          if (tap == 0 || kc == tc.kc_begin) {
+            const int ws = wc & 1;
+            ++wc;
+            if (ws == group) {
+              TW(2, mbar_wait(smem_u32(&wfull_bar[ws]), ((wc - 1) >> 1) & 1));
+              uint8_t* wraw = win_base + ws * win_slot;
+              split_small_only(reinterpret_cast<const uint32_t*>(wraw), reinterpret_cast<uint32_t*>(wraw + win_bytes),
+                               win_bytes / 4, gt, 256);
+              fence_proxy_async_smem();
+              TW(3, named_bar_sync(2 + group, 256));
+              if (gt == 0) {
+                if (CG == 2 && !leader) mbar_arrive_cluster(wsmall_leader + ws * 8);
+                else mbar_arrive(smem_u32(&wsmall_bar[ws]));
+              }
+            }
+          }
+          if ((it % kSplitGroups) == group) {
+            TW(1, mbar_wait(smem_u32(&full_bar[s]), ph));
+            uint8_t* base = smem + s * C::STAGE_BYTES;
+            split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_OFF),
+                             reinterpret_cast<uint32_t*>(base + C::A_OFF + C::B_BYTES), C::B_ROWS * BK, gt, 256);
+            fence_proxy_async_smem();
+            TW(3, named_bar_sync(2 + group, 256));
+            if (gt == 0) {
+              if (CG == 2 && !leader) mbar_arrive_cluster(conv_leader + s * 8);
+              else mbar_arrive(smem_u32(&conv_bar[s]));
+            }
+          }
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    } else
     for (int t = cluster_id; t < n_tiles_total; t += n_clusters) {
       const TileCoord tc = decode_tile(g, t, BN, CG);
       int tap = 0;  // WIN: tap of the current k-chunk (tap innermost), advanced without division
@@ -1274,7 +1347,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
             wwaited = true;
           }
           // row ct of this tap's tile = window row ct + shift(tap) - min shift
-          load_a_half_kmajor(win_base + wslot * win_bytes, ct + s_off[0][tap] - g.win_off_min, half, v);
+          load_a_half_kmajor(win_base + wslot * win_slot, ct + s_off[0][tap] - g.win_off_min, half, v);
         } else if constexpr (A_MN) {
           load_a_half_mnmajor(base, ct, half, v);
         } else {
@@ -1286,6 +1359,13 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           w[j] = __float_as_uint(__uint_as_float(v[j]) - __uint_as_float(big));
           if constexpr (!C::A_SS) v[j] = big;
         }
+#if WAP_B_SPLIT_EARLY
+        // B's small half first: it needs no TMEM slot, so the only work left between the
+        // slot wait (MMA completion of the slot's previous step) and this step's conv_bar
+        // arrival is the A store
+        split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_OFF),
+                         reinterpret_cast<uint32_t*>(base + C::A_OFF + C::B_BYTES), C::B_ROWS * BK, gt, 256);
+#endif
         // TMEM A slot of this step: free once the MMAs of its previous use committed
         const int aj = it % C::A_SLOTS;
         TW(2, mbar_wait(smem_u32(&aslot_bar[aj]), ((it / C::A_SLOTS) & 1) ^ 1));
@@ -1299,8 +1379,10 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           tmem_st_32x32b_x16(acol + 32, w);
         }
 #endif
+#if !WAP_B_SPLIT_EARLY
         split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_OFF),
                          reinterpret_cast<uint32_t*>(base + C::A_OFF + C::B_BYTES), C::B_ROWS * BK, gt, 256);
+#endif
         TW(3, tmem_st_wait());
         tc_fence_before();
         fence_proxy_async_smem();
@@ -1339,7 +1421,8 @@ constexpr int kExclusiveSmem = 120 * 1024;  // > half of the 228 KB per SM: one 
 // dynamic shared memory of one launch (WIN adds the two A halo windows)
 template <int BN, int PREC, int CG, bool WIN>
 constexpr int smem_bytes_for(int win_boxes) {
-  return Cfg<BN, PREC, CG, WIN>::SMEM + (WIN ? 2 * win_boxes * Cfg<BN, PREC, CG, WIN>::A_BYTES : 0);
+  return Cfg<BN, PREC, CG, WIN>::SMEM +
+         (WIN ? 2 * win_boxes * Cfg<BN, PREC, CG, WIN>::A_BYTES * Cfg<BN, PREC, CG, WIN>::WIN_MUL : 0);
 }
 
 template <int BN, bool AMN, bool BMN, int PREC, int CG, bool WIN = false>
