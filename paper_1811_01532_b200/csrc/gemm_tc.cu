@@ -250,7 +250,11 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
     // (one accumulator buffer with BN = 192: the MMAs wait for each 192-column drain, so
     // 2x longer chains; measured AlexNet conv2: 613 / 668 / 737 tensor-pipe TF/s at chains
     // of 8 / 16 / unbounded, tools/gpurun/r2_exp1.sh)
-    g.chain_chunks = cc ? std::max(0, atoi(cc)) : (s.bn == 192 ? 2 * kChainChunks : kChainChunks);
+    // The N = 64 pair kernels (one CTA) hold one accumulator next to S as well and issue 2
+    // MMAs per k-slice instead of 3, so 16 k-chunks is the same MMA count per chain as 8
+    // (AlexNet d_pool1: 493 / 517 / 533 TF/s at chains of 8 / 16 / unbounded, r2_exp2.sh)
+    const bool pair = s.bn == 64 && s.cg == 1 && WAP_N64_PAIR;
+    g.chain_chunks = cc ? std::max(0, atoi(cc)) : ((s.bn == 192 || pair) ? 2 * kChainChunks : kChainChunks);
   }
   g.mbits_out = d.mbits_out;
   g.mbits_out_ld = d.mbits_out_ld;
