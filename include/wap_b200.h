@@ -92,7 +92,7 @@ int wap_gemm_plan_run(void* plan, void* stream);
 void wap_gemm_plan_destroy(void* plan);
 /* The launch configuration a plan resolved to, and the part of it that fixes the fp32
  * rounding: out[0..7] = {block_n, cta_group, splits, k_chunks_per_split, window boxes,
- * precision, n64 pair mode, accumulator chain length in k-chunks}. Two plans of one descriptor with equal
+ * precision, n64 pair mode (1: one CTA, 2: CTA pair), accumulator chain length in k-chunks}. Two plans of one descriptor with equal
  * {splits, k_chunks_per_split, precision, cta_group, pair mode, window > 0, chain} produce bitwise-equal outputs
  * (same per-element accumulation order); the runtime's autotuner only chooses among
  * those, so tuning never changes results (tests/test_gemm_gpu.py). */

@@ -253,7 +253,7 @@ int build_plan(const wap_gemm_desc_t* desc, Plan* p) {
     // The N = 64 pair kernels (one CTA) hold one accumulator next to S as well and issue 2
     // MMAs per k-slice instead of 3, so 16 k-chunks is the same MMA count per chain as 8
     // (AlexNet d_pool1: 493 / 517 / 533 TF/s at chains of 8 / 16 / unbounded, r2_exp2.sh)
-    const bool pair = s.bn == 64 && s.cg == 1 && WAP_N64_PAIR;
+    const bool pair = s.bn == 64 && ((s.cg == 1 && WAP_N64_PAIR) || (s.cg == 2 && WAP_N64_PAIR2));
     g.chain_chunks = cc ? std::max(0, atoi(cc)) : ((s.bn == 192 || pair) ? 2 * kChainChunks : kChainChunks);
   }
   g.mbits_out = d.mbits_out;
@@ -358,7 +358,7 @@ extern "C" int wap_gemm_plan_info(const void* plan, int64_t out[8]) {
   out[3] = p.args.k_chunks_per_split;
   out[4] = p.args.win_boxes;
   out[5] = p.prec;
-  out[6] = (p.prec == 3 && p.bn == 64 && p.cg == 1 && WAP_N64_PAIR) ? 1 : 0;
+  out[6] = (p.prec == 3 && p.bn == 64) ? ((p.cg == 1 && WAP_N64_PAIR) ? 1 : ((p.cg == 2 && WAP_N64_PAIR2) ? 2 : 0)) : 0;
   out[7] = p.args.chain_chunks;
   return WAP_OK;
 }

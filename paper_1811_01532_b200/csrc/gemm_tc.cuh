@@ -45,6 +45,9 @@ constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap
 #ifndef WAP_N64_PAIR
 #define WAP_N64_PAIR 1
 #endif
+#ifndef WAP_N64_PAIR2
+#define WAP_N64_PAIR2 1
+#endif
 // Split accumulators (3xTF32): the tcgen05 MMA rounds its accumulator toward zero,
 // about one ulp of the accumulator per MMA (tools/gemm_split_acc.py: bias
 // -6.7e-9 * K relative, linear in the MMAs per accumulator, for exact-in-tf32
@@ -130,8 +133,16 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = B_ROWS * BK * 4;
   static constexpr int A_OFF = WIN ? 0 : A_BYTES;  // B offset inside a stage
-  // PREC 3 smem stage: [A raw] | B raw | B small
-  static constexpr int STAGE_BYTES = PREC == 3 ? (A_OFF + 2 * B_BYTES) : (A_BYTES + B_BYTES);
+  // PAIR2 (3xTF32, N = 64, CTA pair): the pair-mode N = 128 MMA [B_raw | B_small] with the
+  // B operand's two halves in the two CTAs: CTA 0 stages B_raw (64 rows) in region P, CTA 1
+  // B_small (64 rows, split from its raw copy in region R) in P; the N = 64 small*B MMA takes
+  // B_raw rows 0-31 from CTA 0's region Q and rows 32-63 from CTA 1's. 2 MMAs per k-slice
+  // like PAIR, with the CTA pair's shared A/B traffic and two accumulators.
+  static constexpr bool PAIR2 = PREC == 3 && BN == 64 && CG == 2 && WAP_N64_PAIR2;
+  static constexpr int P2_Q = 64 * 128, P2_R = 96 * 128;  // PAIR2 region offsets after P
+  // PREC 3 smem stage: [A raw] | B raw | B small   (PAIR2: [A raw] | P | Q | R)
+  static constexpr int B_REGION = PAIR2 ? 160 * 128 : 2 * B_BYTES;
+  static constexpr int STAGE_BYTES = PREC == 3 ? (A_OFF + B_REGION) : (A_BYTES + B_BYTES);
   // two accumulators (epilogue overlap) only if >= 4 A stages still fit in TMEM
   // PAIR (3xTF32, N = 64, one CTA): a tcgen05 MMA with N <= 64 costs about as much as
   // N = 108 (tools/mma_probe.cu: ~54 cycles vs 32 at full rate), so big*big and
@@ -146,13 +157,14 @@ struct Cfg {
   // 64-column A slots, so those kernels hold one accumulator buffer next to S
   static constexpr bool A_SS = WAP_A_SS && PREC == 3 && !(CG == 1 && BN == 64);
   static constexpr bool SACC = PREC == 3 && !PAIR && WAP_SPLIT_ACC && !A_SS;
-  static constexpr int HALF = PAIR ? 64 : BN;                      // column offset of half 1
-  static constexpr int ACC_W = PAIR ? 128 : (SACC ? 2 * BN : BN);  // TMEM columns per accumulator
+  static constexpr bool HALVES = PAIR || PAIR2 || SACC;             // accumulator has two halves to add
+  static constexpr int HALF = (PAIR || PAIR2) ? 64 : BN;            // column offset of half 1
+  static constexpr int ACC_W = (PAIR || PAIR2) ? 128 : (SACC ? 2 * BN : BN);  // TMEM columns per accumulator
   // TMEM columns of one A slot: big + small (TS big*B), or small only when the MMAs
   // that use A's high part read the raw tile from shared memory (WAP_A_SS)
   static constexpr int A_SLOT_W = A_SS ? 32 : 64;
   // running sum of the accumulator chains (3xTF32, see GemmArgs::chain_chunks): BN columns
-  static constexpr int S_W = PREC == 3 ? (PAIR ? 64 : BN) : 0;
+  static constexpr int S_W = PREC == 3 ? ((PAIR || PAIR2) ? 64 : BN) : 0;
   // WSS (halo window, CTA pair): the small half of the whole A window is computed once
   // per channel chunk into shared memory next to the raw window, and all three MMAs
   // of every tap read A from the window (SS): no per-tap A split, no TMEM A slots
@@ -675,6 +687,19 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         for (int j = 0; j < NA; ++j) mn_box(g.a, s_off[0], a_row0 + 32 * j, ac0[j], ao[j]);
 #pragma unroll
         for (int j = 0; j < NB; ++j) mn_box(g.b, s_off[1], b_row0 + 32 * j, bc0[j], bo[j]);
+        // PAIR2: B boxes 0, 1 = rows n0 .. n0+63 (CTA 0 -> P, CTA 1 -> R), box 2 = this CTA's
+        // 32-row half (-> Q); MN-major: inner coordinate + k offset of each 32-row box
+        int p2row[3], p2c0[3], p2o[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          p2row[j] = tc.n0 + (j < 2 ? 32 * j : 32 * (int)rank);
+          p2c0[j] = 0;
+          p2o[j] = 0;
+          if constexpr (C::PAIR2 && B_MN) mn_box(g.b, s_off[1], p2row[j], p2c0[j], p2o[j]);
+        }
+        auto p2dst = [&](int st, int j) -> uint32_t {
+          return j < 2 ? stage_b(st) + (rank == 0 ? 0 : C::P2_R) + j * 4096 : stage_b(st) + C::P2_Q;
+        };
         // K-major operands: (tap, k within tap) advance with k
         int k = tc.kc_begin * BK;
         int a_tap = 0, a_kin = k, b_tap = 0, b_kin = k;
@@ -697,9 +722,16 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
             }
             TW(2, mbar_wait(smem_u32(&empty_bar[s]), ph ^ 1));
             const uint32_t fb = smem_u32(&full_bar[s]);
-            mbar_arrive_expect_tx(fb, C::B_BYTES);
+            mbar_arrive_expect_tx(fb, C::PAIR2 ? 3 * 4096 : C::B_BYTES);
             const int kflat = w_tap * tpa + w_cidx * BK;
-            if constexpr (B_MN) {
+            if constexpr (C::PAIR2) {
+#pragma unroll
+              for (int j = 0; j < 3; ++j) {
+                if constexpr (B_MN) tma_load<1>(p2dst(s, j), &tmB, fb, p2c0[j], kflat + p2o[j]);
+                else if (tpb > 0) tma_load<1>(p2dst(s, j), &tmB, fb, w_cidx * BK, p2row[j] + s_off[1][w_tap]);
+                else tma_load<1>(p2dst(s, j), &tmB, fb, kflat, p2row[j] + (b_row - b_row0));
+              }
+            } else if constexpr (B_MN) {
 #pragma unroll
               for (int j = 0; j < NB; ++j) tma_load<1>(stage_b(s) + j * (BK * 128), &tmB, fb, bc0[j], kflat + bo[j]);
             } else if (tpb > 0) {  // host guarantees tpb == tpa: the B tap is the A tap
@@ -721,7 +753,13 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
             } else {
               tma_load<CGT>(stage_a(s), &tmA, fb, a_kin, a_row);
             }
-            if constexpr (B_MN) {
+            if constexpr (C::PAIR2) {
+#pragma unroll
+              for (int j = 0; j < 3; ++j) {
+                if constexpr (B_MN) tma_load<CGT>(p2dst(s, j), &tmB, fb, p2c0[j], k + p2o[j]);
+                else tma_load<CGT>(p2dst(s, j), &tmB, fb, b_kin, p2row[j] + (b_row - b_row0));
+              }
+            } else if constexpr (B_MN) {
 #pragma unroll
               for (int j = 0; j < NB; ++j) tma_load<CGT>(stage_b(s) + j * (BK * 128), &tmB, fb, bc0[j], k + bo[j]);
             } else {
@@ -733,7 +771,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
             if (leader) mbar_arrive_expect_tx(fb, 2 * (C::A_BYTES + C::B_BYTES));
             issue(std::integral_constant<int, 2>{});
           } else {
-            mbar_arrive_expect_tx(fb, C::A_BYTES + C::B_BYTES);
+            mbar_arrive_expect_tx(fb, C::A_BYTES + (C::PAIR2 ? 3 * 4096 : C::B_BYTES));
             TW(3, issue(std::integral_constant<int, 1>{}));
           }
           // L2 prefetch g.l2_prefetch k-steps ahead of the smem ring for operands without
@@ -846,7 +884,17 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
             for (int kk = 0; kk < BK / 8; ++kk) {
               const uint64_t bd = bd0 + kk * kB;
               const uint32_t first = kk > 0 ? 1u : first0;
-              if constexpr (C::WSS) {
+              if constexpr (C::PAIR2) {
+                constexpr uint32_t idesc1 = make_idesc_tf32(BM * CG, 128, A_MN, B_MN);
+                constexpr uint32_t idesc2 = make_idesc_tf32(BM * CG, 64, C::WSS ? A_MN : false, B_MN);
+                const uint64_t ad = ad0 + kk * kA;
+                const uint64_t bq = operand_desc<B_MN>(stage_b(s) + C::P2_Q, 0) + kk * kB;
+                umma_cg<CG>(dacc_cur, ad, bd, idesc1, first);                  // A * [B | B_small] (pair halves)
+                if constexpr (C::WSS)
+                  umma_cg<CG>(dacc_cur, ad + (uint64_t)(win_bytes >> 4), bq, idesc2, 1u);  // small * B (window)
+                else
+                  umma_ts_cg<CG>(dacc_cur, a_big0 + kk * 8, bq, idesc2, 1u);  // small * B (TMEM A)
+              } else if constexpr (C::WSS) {
                 // all SS: small half of the window at win_bytes past the raw window
                 const uint64_t ad = ad0 + kk * kA;
                 const uint64_t as = ad + (uint64_t)(win_bytes >> 4);
@@ -959,7 +1007,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
     // logical accumulator columns [c0, c0 + 32) of buffer `a` (PAIR / SACC: both halves added)
     auto load_acc = [&](int a, int c0, uint32_t (&v)[32]) {
       tmem_ld_32x32b_x32(lane_tm + a * C::ACC_W + c0, v);
-      if constexpr (C::PAIR || C::SACC) {
+      if constexpr (C::HALVES) {
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           uint32_t v2[16];
@@ -988,9 +1036,9 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         for (int c0 = 0; c0 < C::S_W; c0 += 16) {
           uint32_t v[16], w[16];
           tmem_ld_32x32b_x16(lane_tm + acc * C::ACC_W + c0, v);
-          if constexpr (C::PAIR || C::SACC) tmem_ld_32x32b_x16(lane_tm + acc * C::ACC_W + C::HALF + c0, w);
+          if constexpr (C::HALVES) tmem_ld_32x32b_x16(lane_tm + acc * C::ACC_W + C::HALF + c0, w);
           tmem_ld_wait();
-          if constexpr (C::PAIR || C::SACC) {
+          if constexpr (C::HALVES) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
           }
@@ -1251,6 +1299,17 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
     const int gt = (sw & 7) * 32 + lane;  // thread index inside the group (0..255)
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t conv_leader = CG == 2 ? map_to_rank(smem_u32(&conv_bar[0]), 0) : smem_u32(&conv_bar[0]);
+    // B's small half of a landed stage (PAIR2: only CTA 1, from its raw copy R into P)
+    auto split_b = [&](uint8_t* base) {
+      if constexpr (C::PAIR2) {
+        if (rank == 1)
+          split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_OFF + C::P2_R),
+                           reinterpret_cast<uint32_t*>(base + C::A_OFF), 64 * BK, gt, 256);
+      } else {
+        split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_OFF),
+                         reinterpret_cast<uint32_t*>(base + C::A_OFF + C::B_BYTES), C::B_ROWS * BK, gt, 256);
+      }
+    };
     int s = 0;
     uint32_t ph = 0;
     int it = 0;
@@ -1284,8 +1343,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           if ((it % kSplitGroups) == group) {
             TW(1, mbar_wait(smem_u32(&full_bar[s]), ph));
             uint8_t* base = smem + s * C::STAGE_BYTES;
-            split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_OFF),
-                             reinterpret_cast<uint32_t*>(base + C::A_OFF + C::B_BYTES), C::B_ROWS * BK, gt, 256);
+            split_b(base);
             fence_proxy_async_smem();
             TW(3, named_bar_sync(2 + group, 256));
             if (gt == 0) {
@@ -1363,8 +1421,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         // B's small half first: it needs no TMEM slot, so the only work left between the
         // slot wait (MMA completion of the slot's previous step) and this step's conv_bar
         // arrival is the A store
-        split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_OFF),
-                         reinterpret_cast<uint32_t*>(base + C::A_OFF + C::B_BYTES), C::B_ROWS * BK, gt, 256);
+        split_b(base);
 #endif
         // TMEM A slot of this step: free once the MMAs of its previous use committed
         const int aj = it % C::A_SLOTS;
@@ -1380,8 +1437,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         }
 #endif
 #if !WAP_B_SPLIT_EARLY
-        split_small_only(reinterpret_cast<const uint32_t*>(base + C::A_OFF),
-                         reinterpret_cast<uint32_t*>(base + C::A_OFF + C::B_BYTES), C::B_ROWS * BK, gt, 256);
+        split_b(base);
 #endif
         TW(3, tmem_st_wait());
         tc_fence_before();

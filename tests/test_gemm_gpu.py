@@ -166,3 +166,42 @@ def test_conv_mask_bits_splitk(cuda, splits, Co):
     ref_dx = (xd.grad * (xd > 0)).permute(0, 2, 3, 1)
     assert dev(dx_b[:, :H, :W], ref_dx) < TOL[3] and dev(dx_f[:, :H, :W], ref_dx) < TOL[3]
     assert dx_b[:, H:].abs().max().item() == 0 and dx_b[:, :, W:].abs().max().item() == 0
+
+
+@pytest.mark.parametrize("cluster", [1, 2])
+@pytest.mark.parametrize("window", [0, -1])
+def test_n64_pair_modes(cuda, cluster, window):
+    """N = 64 3xTF32 GEMMs in every pair form: one CTA (PAIR: [B | B_small] as one N = 128 MMA)
+    and a CTA pair (PAIR2: B_raw in CTA 0, B_small in CTA 1), with and without the halo
+    window, for a conv fprop (B MN-major, Co = 64) and a dgrad (B K-major, Ci = 64), long
+    enough in K to run several accumulator chains."""
+    Bn, H, Ci, Co, k = 2, 27, 64, 64, 5
+    p = k // 2
+    W = H
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.relu(torch.randn(Bn, H, W, Ci, device=cuda, generator=g))
+    w = torch.randn(k, k, Ci, Co, device=cuda, generator=g) * 0.1
+    xp = _pad(x, p)
+
+    def run(call):
+        d = type(call.desc).from_buffer_copy(call.desc)
+        d.cluster, d.window = cluster, window
+        d.workspace, d.workspace_bytes = None, 0
+        c = K.GemmCall(d)
+        c()
+        return c.info()
+
+    yp = torch.full((Bn, H + p, W + p, Co), float("nan"), device=cuda)
+    info = run(K.conv_fprop(xp, w, yp, B=Bn, H=H, W=W, Ci=Ci, Co=Co, k=k, pad=p, precision=3, run=False))
+    assert info["block_n"] == 64 and info["cta_group"] == cluster and info["pair"] == cluster
+    dy = torch.randn(Bn, H, W, Co, device=cuda, generator=g)
+    dyp = _pad(dy, p)
+    dxp = torch.full_like(xp, float("nan"))
+    run(K.conv_dgrad(dyp, w, dxp, B=Bn, H=H, W=W, Ci=Ci, Co=Co, k=k, pad=p, precision=3, run=False))
+    torch.cuda.synchronize()
+    xd = x.double().permute(0, 3, 1, 2).requires_grad_(True)
+    wd = w.double().permute(3, 2, 0, 1)
+    out = F.conv2d(xd, wd, padding=p)
+    out.backward(dy.double().permute(0, 3, 1, 2))
+    assert dev(yp[:, :H, :W], out.detach().permute(0, 2, 3, 1)) < TOL[3]
+    assert dev(dxp[:, :H, :W], xd.grad.permute(0, 2, 3, 1)) < TOL[3]
