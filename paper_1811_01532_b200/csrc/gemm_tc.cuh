@@ -48,6 +48,9 @@ constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap
 #ifndef WAP_N64_PAIR2
 #define WAP_N64_PAIR2 1
 #endif
+#ifndef WAP_PAIR_ONE_GROUP
+#define WAP_PAIR_ONE_GROUP 1
+#endif
 // Split accumulators (3xTF32): the tcgen05 MMA rounds its accumulator toward zero,
 // about one ulp of the accumulator per MMA (tools/gemm_split_acc.py: bias
 // -6.7e-9 * K relative, linear in the MMAs per accumulator, for exact-in-tf32
@@ -150,6 +153,14 @@ struct Cfg {
   // stage into a 128-column accumulator, and small*big as an N = 64 MMA into its
   // first half; the epilogue adds the two halves. 2 MMAs per k-slice instead of 3.
   static constexpr bool PAIR = PREC == 3 && BN == 64 && CG == 1 && WAP_N64_PAIR;
+  // splitter groups: the single-CTA pair kernels run ONE group (its per-step work is small)
+  // so their TMEM A-slot ring needs no even length: 3 slots of 64 columns fit next to two
+  // 128-column accumulators and S, and the chain drains overlap the MMAs
+  // (halo-window pair kernels keep two groups: their per-tap A split measured too much for
+  // one group, d_pool1 0.386 -> 0.427 ms; without the window one group wins, VGG conv1_2
+  // fprop / dgrad 0.96 / 1.12 -> 0.66 / 0.75 ms, r2_exp8.sh)
+  static constexpr int SG = (PAIR && !WIN && WAP_PAIR_ONE_GROUP) ? 1 : kSplitGroups;
+  static constexpr int MIN_SLOTS = SG == 1 ? 3 : WAP_MIN_A_SLOTS;
   // SACC: two-half accumulators (big*big | small products); PAIR always has two halves
   // raw A from shared memory except for the single-CTA N = 64 pair kernels, where the
   // N = 128 SS MMA (A + all of [B | B_small] from this CTA's shared memory, ~128 B/clk)
@@ -172,7 +183,7 @@ struct Cfg {
   static constexpr int WIN_MUL = WSS ? 2 : 1;  // window slot = raw (| small)
   static constexpr int ACC_BUFS =
       WSS ? ((2 * ACC_W + S_W <= 512) ? 2 : 1)
-          : ((PREC == 3 && 512 - 2 * ACC_W - S_W < WAP_MIN_A_SLOTS * A_SLOT_W) ? 1 : 2);
+          : ((PREC == 3 && 512 - 2 * ACC_W - S_W < MIN_SLOTS * A_SLOT_W) ? 1 : 2);
   static constexpr int S_COL = ACC_BUFS * ACC_W;
   static constexpr int A_COL0 = S_COL + S_W;
   static constexpr int TMEM_A_SLOTS = PREC == 3 ? (512 - A_COL0) / A_SLOT_W : 64;
@@ -194,7 +205,7 @@ struct Cfg {
 #define WAP_RING_EVEN 1
 #endif
   static constexpr int ring_round(int n) {
-    return (PREC == 3 && WAP_RING_EVEN) ? n / kSplitGroups * kSplitGroups : n;
+    return (PREC == 3 && WAP_RING_EVEN) ? n / SG * SG : n;
   }
   static constexpr int A_SLOTS =
       PREC == 3 ? ring_round(TMEM_A_SLOTS > WAP_MAX_A_SLOTS ? WAP_MAX_A_SLOTS : TMEM_A_SLOTS) : 1;
@@ -203,15 +214,15 @@ struct Cfg {
   static constexpr int STAGES = WIN ? ((WIN && A_SS && WAP_WIN_SMALL && BN <= 128) ? 4 : 6)
                                     : ring_round(STAGES_SMEM > 8 ? 8 : STAGES_SMEM);
   static constexpr int TMEM_COLS = PREC == 3 ? 512 : ((2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512));
-  static constexpr int THREADS = PREC == 3 ? 256 + 256 * kSplitGroups : 256;  // + splitter warp groups
+  static constexpr int THREADS = PREC == 3 ? 256 + 256 * SG : 256;  // + splitter warp groups
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + kEpiStage + kBarBytes;
   static_assert(STAGES >= 2, "need at least two pipeline stages");
-  static_assert(PREC != 3 || !WAP_RING_EVEN || (STAGES % kSplitGroups == 0 && A_SLOTS % kSplitGroups == 0),
+  static_assert(PREC != 3 || !WAP_RING_EVEN || (STAGES % SG == 0 && A_SLOTS % SG == 0),
                 "3xTF32 rings must be multiples of the splitter group count");
   static_assert(B_ROWS % 32 == 0, "B rows per CTA must be a multiple of 32");
-  static_assert(PREC != 3 || A_SLOTS >= kSplitGroups, "3xTF32 needs TMEM A slots next to the accumulators");
+  static_assert(PREC != 3 || A_SLOTS >= SG, "3xTF32 needs TMEM A slots next to the accumulators");
   static_assert(PREC != 3 || WSS || A_COL0 + A_SLOTS * A_SLOT_W <= 512, "3xTF32 TMEM layout exceeds 512 columns");
-  static_assert(!WSS || kSplitGroups == 2, "WSS assigns window slot g to splitter group g");
+  static_assert(!WSS || SG == 2, "WSS assigns window slot g to splitter group g");
 };
 
 // A row m (32 k-values) of a landed stage, K-major SWIZZLE_128B tile.
@@ -648,7 +659,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         mbar_init(smem_u32(&wfull_bar[i]), 1);
         // every splitter group, plus (WAP_A_SS) the MMA commit of the window's last tap;
         // WSS: the MMA commit alone (the owning group's window read precedes wsmall)
-        mbar_init(smem_u32(&wempty_bar[i]), C::WSS ? 1 : kSplitGroups + (C::A_SS ? 1 : 0));
+        mbar_init(smem_u32(&wempty_bar[i]), C::WSS ? 1 : C::SG + (C::A_SS ? 1 : 0));
         mbar_init(smem_u32(&wsmall_bar[i]), CG);  // WSS: one arrive per CTA of the pair
       }
     }
@@ -1340,7 +1351,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
               }
             }
           }
-          if ((it % kSplitGroups) == group) {
+          if ((it % C::SG) == group) {
             TW(1, mbar_wait(smem_u32(&full_bar[s]), ph));
             uint8_t* base = smem + s * C::STAGE_BYTES;
             split_b(base);
@@ -1373,10 +1384,10 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           }
           last_in_win = (tap == ntaps - 1) || (kc == tc.kc_end - 1);
         }
-        if ((it % kSplitGroups) != group) {
+        if ((it % C::SG) != group) {
           // observe this step's stage / A-slot phases (no work) so that the parity
           // waits of this group's own later steps never skip a phase
-          if (!WAP_RING_EVEN && (STAGES % kSplitGroups != 0 || C::A_SLOTS % kSplitGroups != 0)) {
+          if (!WAP_RING_EVEN && (STAGES % C::SG != 0 || C::A_SLOTS % C::SG != 0)) {
             mbar_wait(smem_u32(&full_bar[s]), ph);
             mbar_wait(smem_u32(&aslot_bar[it % C::A_SLOTS]), ((it / C::A_SLOTS) & 1) ^ 1);
           }
