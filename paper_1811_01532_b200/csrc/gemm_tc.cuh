@@ -51,6 +51,9 @@ constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap
 #ifndef WAP_PAIR_ONE_GROUP
 #define WAP_PAIR_ONE_GROUP 1
 #endif
+#ifndef WAP_PAIR_SS
+#define WAP_PAIR_SS 0
+#endif
 // Split accumulators (3xTF32): the tcgen05 MMA rounds its accumulator toward zero,
 // about one ulp of the accumulator per MMA (tools/gemm_split_acc.py: bias
 // -6.7e-9 * K relative, linear in the MMAs per accumulator, for exact-in-tf32
@@ -166,7 +169,7 @@ struct Cfg {
   // N = 128 SS MMA (A + all of [B | B_small] from this CTA's shared memory, ~128 B/clk)
   // measured slower than the TS form (tools/gpurun/r2_exp1.sh, r02); the TS form keeps
   // 64-column A slots, so those kernels hold one accumulator buffer next to S
-  static constexpr bool A_SS = WAP_A_SS && PREC == 3 && !(CG == 1 && BN == 64);
+  static constexpr bool A_SS = WAP_A_SS && PREC == 3 && !(CG == 1 && BN == 64 && !WAP_PAIR_SS);
   static constexpr bool SACC = PREC == 3 && !PAIR && WAP_SPLIT_ACC && !A_SS;
   static constexpr bool HALVES = PAIR || PAIR2 || SACC;             // accumulator has two halves to add
   static constexpr int HALF = (PAIR || PAIR2) ? 64 : BN;            // column offset of half 1
@@ -179,7 +182,7 @@ struct Cfg {
   // WSS (halo window, CTA pair): the small half of the whole A window is computed once
   // per channel chunk into shared memory next to the raw window, and all three MMAs
   // of every tap read A from the window (SS): no per-tap A split, no TMEM A slots
-  static constexpr bool WSS = WIN && A_SS && WAP_WIN_SMALL && BN <= 128;
+  static constexpr bool WSS = WIN && A_SS && WAP_WIN_SMALL && BN <= 128 && !PAIR;
   static constexpr int WIN_MUL = WSS ? 2 : 1;  // window slot = raw (| small)
   static constexpr int ACC_BUFS =
       WSS ? ((2 * ACC_W + S_W <= 512) ? 2 : 1)
@@ -211,7 +214,7 @@ struct Cfg {
       PREC == 3 ? ring_round(TMEM_A_SLOTS > WAP_MAX_A_SLOTS ? WAP_MAX_A_SLOTS : TMEM_A_SLOTS) : 1;
   // (WSS: the small window doubles the window footprint; 4 B stages keep one window pair
   // of 2 boxes + stages + epilogue staging under 227 KB for BN <= 128)
-  static constexpr int STAGES = WIN ? ((WIN && A_SS && WAP_WIN_SMALL && BN <= 128) ? 4 : 6)
+  static constexpr int STAGES = WIN ? (WSS ? 4 : 6)
                                     : ring_round(STAGES_SMEM > 8 ? 8 : STAGES_SMEM);
   static constexpr int TMEM_COLS = PREC == 3 ? 512 : ((2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512));
   static constexpr int THREADS = PREC == 3 ? 256 + 256 * SG : 256;  // + splitter warp groups

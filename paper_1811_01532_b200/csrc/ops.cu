@@ -5,6 +5,9 @@
 // reductions deterministic (fixed order, no atomics) so replicas stay bitwise equal.
 #include <atomic>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "../../include/wap_b200.h"
 
@@ -1216,6 +1219,89 @@ __global__ void __launch_bounds__(256) lrn_maxpool_fwd_kernel(const float* __res
   }
 }
 
+// Row-band form of the fused LRN -> MaxPool forward: a block owns image b and pooled rows
+// [ho0, ho0 + R); it computes the LRN of every input pixel of rows
+// [ho0*s, (ho0+R-1)*s + WIN) ONCE into shared memory (lrn_lane, so the same floats), then
+// pools from shared memory in maxpool_fwd_kernel's order (rows, then columns; first max
+// wins). Values and argmax are bitwise those of lrn_maxpool_fwd_kernel, which recomputes
+// each LRN up to (WIN/s)^2 = 2.25x for 3/2 windows and measured compute-bound (r01 ncu).
+// Recompute here: (R*s + WIN - s) / (R*s) input rows per pooled row (1.25x at R = 2).
+template <int WIN, int VPL>
+__global__ void __launch_bounds__(256) lrn_maxpool_band_kernel(const float* __restrict__ x, wap_layout_t xl,
+                                                               float alpha, float beta, float k, int s, int R,
+                                                               float* __restrict__ y, wap_layout_t yl,
+                                                               uint8_t* __restrict__ arg) {
+  constexpr int NV = 4 * VPL;
+  constexpr int C = 64 * VPL;
+  extern __shared__ float4 band4[];
+  float* band = reinterpret_cast<float*>(band4);
+  const int lane = threadIdx.x & 31;
+  const int sl = lane & 15;
+  const int c0 = sl * NV;
+  const int hw = threadIdx.x >> 4;  // half-warp 0..15
+  const int bands = (yl.H + R - 1) / R;
+  const int b = blockIdx.x / bands;
+  const int ho0 = (blockIdx.x - b * bands) * R;
+  const int nho = min(R, yl.H - ho0);
+  const int h0 = ho0 * s;
+  const int nrows = min((nho - 1) * s + WIN, xl.H - h0);
+  const int npx = nrows * xl.W;
+  // phase 1: LRN of every input pixel of the band, one half-warp per pixel. The two
+  // half-warps of a warp iterate together (lrn_lane shuffles with the full-warp mask);
+  // the second one idles on the last odd pixel.
+  for (int qb = (hw & ~1); qb < npx; qb += 16) {
+    const int q = qb + (hw & 1);
+    const bool ok = q < npx;
+    const int r = ok ? q / xl.W : 0, w = ok ? q - r * xl.W : 0;
+    float v[NV], o[NV];
+#pragma unroll
+    for (int t = 0; t < VPL; ++t) {
+      float4 xa = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ok) xa = *reinterpret_cast<const float4*>(x + lidx(xl, b, h0 + r, w, c0 + 4 * t));
+      v[4 * t] = xa.x; v[4 * t + 1] = xa.y; v[4 * t + 2] = xa.z; v[4 * t + 3] = xa.w;
+    }
+    lrn_lane<VPL, false>(v, v, sl, alpha, beta, k, o);
+    if (!ok) continue;
+    float* dst = band + (int64_t)q * C + c0;
+#pragma unroll
+    for (int t = 0; t < VPL; ++t)
+      *reinterpret_cast<float4*>(dst + 4 * t) = make_float4(o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
+  }
+  __syncthreads();
+  // phase 2: pooled outputs of the band from shared memory
+  const int nout = nho * yl.W;
+  for (int q = hw; q < nout; q += 16) {
+    const int ro = q / yl.W, wo = q - ro * yl.W;
+    float best[NV];
+    int bi[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) { best[j] = -INFINITY; bi[j] = 0; }
+#pragma unroll
+    for (int a2 = 0; a2 < WIN; ++a2) {
+#pragma unroll
+      for (int bb = 0; bb < WIN; ++bb) {
+        const float* src = band + ((int64_t)(ro * s + a2) * xl.W + wo * s + bb) * C + c0;
+#pragma unroll
+        for (int t = 0; t < VPL; ++t) {
+          const float4 o4 = *reinterpret_cast<const float4*>(src + 4 * t);
+          const float o[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (o[e] > best[4 * t + e]) { best[4 * t + e] = o[e]; bi[4 * t + e] = a2 * WIN + bb; }
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < VPL; ++t) {
+      const int64_t yi = lidx(yl, b, ho0 + ro, wo, c0 + 4 * t);
+      *reinterpret_cast<float4*>(y + yi) = make_float4(best[4 * t], best[4 * t + 1], best[4 * t + 2], best[4 * t + 3]);
+      if (arg)
+        *reinterpret_cast<uchar4*>(arg + yi) = make_uchar4((uint8_t)bi[4 * t], (uint8_t)bi[4 * t + 1],
+                                                           (uint8_t)bi[4 * t + 2], (uint8_t)bi[4 * t + 3]);
+    }
+  }
+}
+
 // Fused MaxPool backward (stride 2) -> LRN backward (size 5) -> GradReLU, for a
 // MaxPool whose input is an LRN output (AlexNet norm1 -> pool1, norm2 -> pool2):
 // a half-warp owns one 2x2 block of pooled-from pixels, lane sl the 4*VPL contiguous
@@ -1712,6 +1798,41 @@ extern "C" int wap_lrn_maxpool_fwd(const float* x, wap_layout_t xl, int size, fl
   int64_t blocks = ((nout + 1) / 2 * 32 + 255) / 256;
   if (blocks > (int64_t)WAP_NUM_SMS * 16) blocks = (int64_t)WAP_NUM_SMS * 16;
   cudaStream_t st = STREAM(stream);
+  // row bands (each input LRN computed ~once) when a band of R >= 1 pooled rows fits in
+  // <= 72 KB of shared memory (3 blocks per SM). Opt-in (WAP_LRN_POOL_BAND=1): measured r02,
+  // AlexNet pool1 0.070 -> 0.084 ms (two serial phases per block, 4 waves), pool2 0.045 ->
+  // 0.043 ms; bitwise equal to the per-output form (tests/test_ops_gpu.py)
+  static const bool band_on = getenv("WAP_LRN_POOL_BAND") && atoi(getenv("WAP_LRN_POOL_BAND")) != 0;
+  int R = 0;
+  for (int r = 4; r >= 1 && band_on; --r) {
+    const int rows = std::min((r - 1) * stride + window, xl.H);
+    if ((int64_t)rows * xl.W * xl.C * 4 <= 72 * 1024) { R = r; break; }
+  }
+  if (R > 0) {
+    const int bands = (yl.H + R - 1) / R;
+    const int rows = std::min((R - 1) * stride + window, xl.H);
+    const size_t smem = (size_t)rows * xl.W * xl.C * 4;
+#define WAP_LRNMPB(WIN, VPL)                                                                                  \
+  do {                                                                                                        \
+    static bool attr = false;                                                                                 \
+    if (!attr) {                                                                                              \
+      WAP_CUDA_TRY(cudaFuncSetAttribute(lrn_maxpool_band_kernel<WIN, VPL>,                                    \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024));             \
+      attr = true;                                                                                            \
+    }                                                                                                         \
+    lrn_maxpool_band_kernel<WIN, VPL><<<yl.B * bands, 256, smem, st>>>(x, xl, alpha, beta, bias, stride, R, y, \
+                                                                       yl, argmax);                          \
+  } while (0)
+    if (window == 3) {
+      if (xl.C == 64) WAP_LRNMPB(3, 1); else WAP_LRNMPB(3, 3);
+    } else {
+      if (xl.C == 64) WAP_LRNMPB(2, 1); else WAP_LRNMPB(2, 3);
+    }
+#undef WAP_LRNMPB
+    WAP_LAUNCH_CHECK();
+    COUNT_LAUNCH();
+    return WAP_OK;
+  }
 #define WAP_LRNMP(WIN, VPL) \
   lrn_maxpool_fwd_kernel<WIN, VPL><<<(int)blocks, 256, 0, st>>>(x, xl, alpha, beta, bias, stride, y, yl, argmax)
   if (window == 3) {
