@@ -54,6 +54,9 @@ constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap
 #ifndef WAP_PAIR_SS
 #define WAP_PAIR_SS 0
 #endif
+#ifndef WAP_PAIR_ODD_RING
+#define WAP_PAIR_ODD_RING 0  // 1 hung a full-size d_pool1 in r02 (tools/gpurun/r2_exp13.sh); off
+#endif
 // Split accumulators (3xTF32): the tcgen05 MMA rounds its accumulator toward zero,
 // about one ulp of the accumulator per MMA (tools/gemm_split_acc.py: bias
 // -6.7e-9 * K relative, linear in the MMAs per accumulator, for exact-in-tf32
@@ -163,7 +166,10 @@ struct Cfg {
   // one group, d_pool1 0.386 -> 0.427 ms; without the window one group wins, VGG conv1_2
   // fprop / dgrad 0.96 / 1.12 -> 0.66 / 0.75 ms, r2_exp8.sh)
   static constexpr int SG = (PAIR && !WIN && WAP_PAIR_ONE_GROUP) ? 1 : kSplitGroups;
-  static constexpr int MIN_SLOTS = SG == 1 ? 3 : WAP_MIN_A_SLOTS;
+  // halo-window pair kernels keep two groups but take an ODD ring of 3 A slots (the groups
+  // then also observe each other's steps, see EVEN): two accumulators + S + 3 x 64 columns
+  static constexpr bool ODD_PAIR = PAIR && WIN && WAP_PAIR_ODD_RING;
+  static constexpr int MIN_SLOTS = (SG == 1 || ODD_PAIR) ? 3 : WAP_MIN_A_SLOTS;
   // SACC: two-half accumulators (big*big | small products); PAIR always has two halves
   // raw A from shared memory except for the single-CTA N = 64 pair kernels, where the
   // N = 128 SS MMA (A + all of [B | B_small] from this CTA's shared memory, ~128 B/clk)
@@ -207,8 +213,9 @@ struct Cfg {
 #ifndef WAP_RING_EVEN
 #define WAP_RING_EVEN 1
 #endif
+  static constexpr bool EVEN = WAP_RING_EVEN && !ODD_PAIR;
   static constexpr int ring_round(int n) {
-    return (PREC == 3 && WAP_RING_EVEN) ? n / SG * SG : n;
+    return (PREC == 3 && EVEN) ? n / SG * SG : n;
   }
   static constexpr int A_SLOTS =
       PREC == 3 ? ring_round(TMEM_A_SLOTS > WAP_MAX_A_SLOTS ? WAP_MAX_A_SLOTS : TMEM_A_SLOTS) : 1;
@@ -220,7 +227,7 @@ struct Cfg {
   static constexpr int THREADS = PREC == 3 ? 256 + 256 * SG : 256;  // + splitter warp groups
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + kEpiStage + kBarBytes;
   static_assert(STAGES >= 2, "need at least two pipeline stages");
-  static_assert(PREC != 3 || !WAP_RING_EVEN || (STAGES % SG == 0 && A_SLOTS % SG == 0),
+  static_assert(PREC != 3 || !EVEN || (STAGES % SG == 0 && A_SLOTS % SG == 0),
                 "3xTF32 rings must be multiples of the splitter group count");
   static_assert(B_ROWS % 32 == 0, "B rows per CTA must be a multiple of 32");
   static_assert(PREC != 3 || A_SLOTS >= SG, "3xTF32 needs TMEM A slots next to the accumulators");
@@ -1390,7 +1397,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
         if ((it % C::SG) != group) {
           // observe this step's stage / A-slot phases (no work) so that the parity
           // waits of this group's own later steps never skip a phase
-          if (!WAP_RING_EVEN && (STAGES % C::SG != 0 || C::A_SLOTS % C::SG != 0)) {
+          if (!C::EVEN && (STAGES % C::SG != 0 || C::A_SLOTS % C::SG != 0)) {
             mbar_wait(smem_u32(&full_bar[s]), ph);
             mbar_wait(smem_u32(&aslot_bar[it % C::A_SLOTS]), ((it / C::A_SLOTS) & 1) ^ 1);
           }
