@@ -1158,13 +1158,25 @@ __global__ void __launch_bounds__(Cfg<BN, PREC, CG, WIN>::THREADS, 1)
           const uint32_t q = lane & 7, r0 = lane >> 3;
           const uint32_t s_even = stg_s + r0 * 128 + ((q ^ r0) << 4);
           const uint32_t s_odd = stg_s + (r0 + 4) * 128 + ((q ^ (r0 + 4)) << 4);
+          // GradReLU mask bits of all 8 rows this lane finishes, loaded up front (8 loads in
+          // flight instead of one round trip per row pair) and packed as 8 nibbles: row it's
+          // 4 columns are bits [4 it, 4 it + 4)
+          uint32_t nib = 0;
+          if (bip) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+              if (row_ok & (1u << r)) nib |= ((__ldg(bip + (int64_t)r * bi4) >> c4) & 0xFu) << (4 * r);
+          }
+          // plain outputs (no bias / ReLU / mask / bits / halo: weight gradients) are already
+          // final in the staging block
+          const bool plain = !bias && !relu && !mask && !g.mbits_in && !bop && g.halo_pad <= 0;
 #pragma unroll 1
-          for (int it = 0; it < 8; it += 2, mp += mp ? 2 * ldm4 : 0, bip += bip ? 2 * bi4 : 0,
+          for (int it = 0; it < (plain ? 0 : 8); it += 2, mp += mp ? 2 * ldm4 : 0,
                    bop += bop ? 2 * bo4 : 0) {
             float4 mk0 = make_float4(1.f, 1.f, 1.f, 1.f), mk1 = mk0;
             if (bip) {
-              const uint32_t w0 = (row_ok & (1u << it)) ? (__ldg(bip) >> c4) : 0u;
-              const uint32_t w1 = (row_ok & (2u << it)) ? (__ldg(bip + bi4) >> c4) : 0u;
+              const uint32_t w0 = (nib >> (4 * it)) & 0xFu;
+              const uint32_t w1 = (nib >> (4 * it + 4)) & 0xFu;
               mk0 = make_float4((float)(w0 & 1u), (float)((w0 >> 1) & 1u), (float)((w0 >> 2) & 1u),
                                 (float)((w0 >> 3) & 1u));
               mk1 = make_float4((float)(w1 & 1u), (float)((w1 >> 1) & 1u), (float)((w1 >> 2) & 1u),
