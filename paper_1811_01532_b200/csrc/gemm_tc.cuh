@@ -54,6 +54,9 @@ constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap
 #ifndef WAP_PAIR_SS
 #define WAP_PAIR_SS 0
 #endif
+#ifndef WAP_PAIR_WIN_MIN_SLOTS
+#define WAP_PAIR_WIN_MIN_SLOTS 2  // windowed pair kernels: 2 even slots + two accumulators (r2_exp17.sh)
+#endif
 #ifndef WAP_PAIR_ODD_RING
 #define WAP_PAIR_ODD_RING 0  // 1 hung a full-size d_pool1 in r02 (tools/gpurun/r2_exp13.sh); off
 #endif
@@ -169,7 +172,8 @@ struct Cfg {
   // halo-window pair kernels keep two groups but take an ODD ring of 3 A slots (the groups
   // then also observe each other's steps, see EVEN): two accumulators + S + 3 x 64 columns
   static constexpr bool ODD_PAIR = PAIR && WIN && WAP_PAIR_ODD_RING;
-  static constexpr int MIN_SLOTS = (SG == 1 || ODD_PAIR) ? 3 : WAP_MIN_A_SLOTS;
+  static constexpr int MIN_SLOTS =
+      (SG == 1 || ODD_PAIR) ? 3 : ((PAIR && WIN) ? WAP_PAIR_WIN_MIN_SLOTS : WAP_MIN_A_SLOTS);
   // SACC: two-half accumulators (big*big | small products); PAIR always has two halves
   // raw A from shared memory except for the single-CTA N = 64 pair kernels, where the
   // N = 128 SS MMA (A + all of [B | B_small] from this CTA's shared memory, ~128 B/clk)
