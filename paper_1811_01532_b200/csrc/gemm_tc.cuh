@@ -54,6 +54,12 @@ constexpr int kBarBytes = 768;  // mbarriers + TMEM address holder [0,512) | tap
 #ifndef WAP_PAIR_SS
 #define WAP_PAIR_SS 0
 #endif
+#ifndef WAP_PAIR_SG3
+#define WAP_PAIR_SG3 0
+#endif
+#ifndef WAP_SG_NARROW
+#define WAP_SG_NARROW 3
+#endif
 #ifndef WAP_PAIR_WIN_MIN_SLOTS
 #define WAP_PAIR_WIN_MIN_SLOTS 2  // windowed pair kernels: 2 even slots + two accumulators (r2_exp17.sh)
 #endif
@@ -168,12 +174,17 @@ struct Cfg {
   // (halo-window pair kernels keep two groups: their per-tap A split measured too much for
   // one group, d_pool1 0.386 -> 0.427 ms; without the window one group wins, VGG conv1_2
   // fprop / dgrad 0.96 / 1.12 -> 0.66 / 0.75 ms, r2_exp8.sh)
-  static constexpr int SG = (PAIR && !WIN && WAP_PAIR_ONE_GROUP) ? 1 : kSplitGroups;
+  // Other kernels with BN <= 128 run THREE groups (1024 threads, 64 registers): measured
+  // r02 (tools/gpurun/r2_exp18.sh) AlexNet conv4 / d_conv3_relu / d_conv4_w 8-10% faster
+  // than two groups (which beat the whole-window split, WSS, as well); BN = 192 keeps two
+  // (three: d_conv2_w 0.30 -> 0.37 ms).
+  static constexpr int SG = PAIR ? (WAP_PAIR_SG3 ? 3 : ((!WIN && WAP_PAIR_ONE_GROUP) ? 1 : kSplitGroups))
+                                 : ((PREC == 3 && BN <= 128) ? WAP_SG_NARROW : kSplitGroups);
   // halo-window pair kernels keep two groups but take an ODD ring of 3 A slots (the groups
   // then also observe each other's steps, see EVEN): two accumulators + S + 3 x 64 columns
   static constexpr bool ODD_PAIR = PAIR && WIN && WAP_PAIR_ODD_RING;
   static constexpr int MIN_SLOTS =
-      (SG == 1 || ODD_PAIR) ? 3 : ((PAIR && WIN) ? WAP_PAIR_WIN_MIN_SLOTS : WAP_MIN_A_SLOTS);
+      (SG == 1 || ODD_PAIR || (PAIR && SG == 3)) ? 3 : ((PAIR && WIN) ? WAP_PAIR_WIN_MIN_SLOTS : WAP_MIN_A_SLOTS);
   // SACC: two-half accumulators (big*big | small products); PAIR always has two halves
   // raw A from shared memory except for the single-CTA N = 64 pair kernels, where the
   // N = 128 SS MMA (A + all of [B | B_small] from this CTA's shared memory, ~128 B/clk)
@@ -192,7 +203,7 @@ struct Cfg {
   // WSS (halo window, CTA pair): the small half of the whole A window is computed once
   // per channel chunk into shared memory next to the raw window, and all three MMAs
   // of every tap read A from the window (SS): no per-tap A split, no TMEM A slots
-  static constexpr bool WSS = WIN && A_SS && WAP_WIN_SMALL && BN <= 128 && !PAIR;
+  static constexpr bool WSS = WIN && A_SS && WAP_WIN_SMALL && BN <= 128 && !PAIR && SG == 2;
   static constexpr int WIN_MUL = WSS ? 2 : 1;  // window slot = raw (| small)
   static constexpr int ACC_BUFS =
       WSS ? ((2 * ACC_W + S_W <= 512) ? 2 : 1)
