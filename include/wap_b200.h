@@ -127,6 +127,14 @@ typedef struct {
 int wap_conv_direct(const float* x, wap_layout_t xl, const float* w, int k, int padding, int ldw,
                     const float* bias, int relu, float* y, wap_layout_t yl, uint32_t* mbits, int64_t mbits_ld,
                     void* stream);
+/* Direct first-layer weight gradient (GradConv2DW, interp.py:82-91) of a 3x3 'same'
+ * stride-1 conv over a 3-channel float4-per-pixel input: dw[(u,v,c), co] (KKIO rows,
+ * row stride ldw) = sum_{b,h,w} x[b,h+u-1,w+v-1,c] * dy[b,h,w,co], fp32 FMAs on CUDA
+ * cores, deterministic (per-band partials in `work`, wap_conv_wgrad_direct_work_floats
+ * floats, summed in band order). Replaces im2col + an M = 27 GEMM (VGG-16 conv1_1). */
+int64_t wap_conv_wgrad_direct_work_floats(wap_layout_t dyl);
+int wap_conv_wgrad_direct(const float* x, wap_layout_t xl, const float* dy, wap_layout_t dyl, int k, int padding,
+                          float* dw, int ldw, float* work, void* stream);
 /* Space-to-depth (first-layer strided conv without im2col): a k x k stride-s conv
  * with padding p over x is a ceil(k/s)^2-tap stride-1 VALID conv over
  *   xs[b, i, j, (dy*s+dx)*C + c] = x[b, s*i+dy-p, s*j+dx-p, c]   (0 outside x)

@@ -142,6 +142,8 @@ _SIGNATURES: list[tuple[str, object, list]] = [
     ("wap_im2col", _I, [_P, wap_layout_t, _I, _I, _I, _I, _I, _I, _P, _I64, _P]),
     ("wap_s2d_input", _I, [_P, wap_layout_t, _I, _I, _I, _I, _P, _I, _P]),
     ("wap_conv_direct", _I, [_P, wap_layout_t, _P, _I, _I, _I, _P, _I, _P, wap_layout_t, _P, _I64, _P]),
+    ("wap_conv_wgrad_direct_work_floats", _I64, [wap_layout_t]),
+    ("wap_conv_wgrad_direct", _I, [_P, wap_layout_t, _P, wap_layout_t, _I, _I, _P, _I, _P, _P]),
     ("wap_s2d_weight", _I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P]),
     ("wap_col2im", _I, [_P, _I64, _I, _I, _I, _I, _I, _I, _P, wap_layout_t, _P, wap_layout_t, _P]),
     ("wap_elementwise", _I, [_I, _P, wap_layout_t, _P, wap_layout_t, _P, _P, wap_layout_t, _P]),

@@ -1621,6 +1621,137 @@ extern "C" int wap_bias_grad(const float* dy, wap_layout_t l, float* db, float* 
   return WAP_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Direct first-layer weight gradient (GradConv2DW, interp.py:82-91) for a 3x3 stride-1
+// conv over a <= 4-channel input (one float4 per pixel): dW[(u,v,c), co] =
+// sum_{b,h,w} x[b, h+u-p, w+v-p, c] * dy[b, h, w, co]. As a GEMM it is M = 27 rows
+// (4.7 of a 128-row tile busy) over K = B*H*W; here each block owns R image rows of one
+// image: the input rows it needs are staged once in shared memory (zero outside the
+// image), thread (co, g) accumulates the 27 sums of output channel co over every 4th
+// pixel g of the band in fp32 FMAs, the 4 pixel groups are summed in a fixed order, and
+// the block writes its [27 x Co] partial; wgrad_direct_final sums the partials in block
+// order (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int kWgdRows = 4;  // image rows per block
+__global__ void __launch_bounds__(256) wgrad_direct_3x3_kernel(const float* __restrict__ x, wap_layout_t xl,
+                                                               const float* __restrict__ dy, wap_layout_t dl,
+                                                               int p, float* __restrict__ part) {
+  extern __shared__ float4 xs[];  // (kWgdRows + 2) rows x (W + 2) pixels
+  const int Co = dl.C;
+  const int W2 = xl.W + 2;
+  const int bands = (dl.H + kWgdRows - 1) / kWgdRows;
+  const int b = blockIdx.x / bands;
+  const int h0 = (blockIdx.x - b * bands) * kWgdRows;
+  const int nr = min(kWgdRows, dl.H - h0);
+  for (int i = threadIdx.x; i < (nr + 2) * W2; i += blockDim.x) {
+    const int r = i / W2, c = i - r * W2;
+    const int h = h0 + r - p, w = c - p;  // input pixel of padded column c, row r
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (h >= 0 && h < xl.H && w >= 0 && w < xl.W) v = *reinterpret_cast<const float4*>(x + lidx(xl, b, h, w, 0));
+    xs[i] = v;
+  }
+  __syncthreads();
+  // thread = (output channel co, pixel group g); Co <= 64 channels per pass
+  const int g = threadIdx.x >> 6;
+  const int co = threadIdx.x & 63;
+  for (int cbase = 0; cbase < Co; cbase += 64) {
+    const int cc = cbase + co;
+    float acc[27];
+#pragma unroll
+    for (int j = 0; j < 27; ++j) acc[j] = 0.f;
+    if (cc < Co) {
+      // pixels w = g, g + 4, ... of each row; the dy loads of 4 pixels are issued together
+      // (one round trip per 4 pixels instead of one per pixel)
+      const int64_t drow = (int64_t)(dl.W + dl.pad) * dl.ld;
+      for (int r = 0; r < nr; ++r) {
+        const float* dyr = dy + lidx(dl, b, h0 + r, 0, cc);
+        const float4* xr = xs + r * W2;
+        for (int w0 = g; w0 < dl.W; w0 += 16) {
+          float d[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) d[i] = (w0 + 4 * i < dl.W) ? __ldg(dyr + (int64_t)(w0 + 4 * i) * dl.ld) : 0.f;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int w = min(w0 + 4 * i, dl.W - 1);  // d = 0 past the row end
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+#pragma unroll
+              for (int v = 0; v < 3; ++v) {
+                const float4 xv = xr[u * W2 + w + v];
+                acc[(u * 3 + v) * 3 + 0] = fmaf(xv.x, d[i], acc[(u * 3 + v) * 3 + 0]);
+                acc[(u * 3 + v) * 3 + 1] = fmaf(xv.y, d[i], acc[(u * 3 + v) * 3 + 1]);
+                acc[(u * 3 + v) * 3 + 2] = fmaf(xv.z, d[i], acc[(u * 3 + v) * 3 + 2]);
+              }
+            }
+          }
+        }
+        (void)drow;
+      }
+    }
+    // sum the 4 pixel groups in order through shared memory (after the staged rows)
+    float* red = reinterpret_cast<float*>(xs + (kWgdRows + 2) * W2);  // [4][27][64]
+#pragma unroll
+    for (int j = 0; j < 27; ++j) red[(g * 27 + j) * 64 + co] = acc[j];
+    __syncthreads();
+    if (g == 0 && cc < Co) {
+#pragma unroll
+      for (int j = 0; j < 27; ++j) {
+        const float t = ((red[j * 64 + co] + red[(27 + j) * 64 + co]) + red[(54 + j) * 64 + co]) +
+                        red[(81 + j) * 64 + co];
+        part[((int64_t)blockIdx.x * 27 + j) * Co + cc] = t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// dw[j, co] = sum over blocks (in block order) of part[blk, j, co]; one warp per (j, co)
+// run of 32 channels, lanes striding the blocks, fixed shuffle tree (deterministic)
+__global__ void wgrad_direct_final_kernel(const float* __restrict__ part, int nblk, int Co, float* __restrict__ dw,
+                                          int ldw) {
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= 27 * Co) return;
+  const int j = wid / Co, co = wid - j * Co;
+  float s = 0.f;
+  for (int k = lane; k < nblk; k += 32) s += part[((int64_t)k * 27 + j) * Co + co];
+  s = warp_sum(s);
+  if (lane == 0) dw[(int64_t)j * ldw + co] = s;
+}
+
+extern "C" int64_t wap_conv_wgrad_direct_work_floats(wap_layout_t dyl) {
+  const int bands = (dyl.H + kWgdRows - 1) / kWgdRows;
+  return (int64_t)dyl.B * bands * 27 * dyl.C;
+}
+
+extern "C" int wap_conv_wgrad_direct(const float* x, wap_layout_t xl, const float* dy, wap_layout_t dyl, int k,
+                                     int padding, float* dw, int ldw, float* work, void* stream) {
+  int rc;
+  if ((rc = check_layout(xl, "x")) || (rc = check_layout(dyl, "dy"))) return rc;
+  WAP_CHECK_ARG(x && dy && dw && work, "conv_wgrad_direct: null pointer");
+  WAP_CHECK_ARG(k == 3 && padding == 1, "conv_wgrad_direct: 3x3 'same' convs only");
+  WAP_CHECK_ARG(xl.ld == 4 && xl.C == 3, "conv_wgrad_direct: input must be one float4 per pixel, 3 channels");
+  WAP_CHECK_ARG(dyl.H == xl.H && dyl.W == xl.W && dyl.B == xl.B && ldw >= dyl.C,
+                "conv_wgrad_direct: shape mismatch");
+  const int bands = (dyl.H + kWgdRows - 1) / kWgdRows;
+  const int64_t nblk = (int64_t)dyl.B * bands;
+  WAP_CHECK_ARG(nblk < (1LL << 31), "conv_wgrad_direct: too many blocks");
+  const size_t smem = (size_t)(kWgdRows + 2) * (xl.W + 2) * 16 + (size_t)4 * 27 * 64 * 4;
+  WAP_CHECK_ARG(smem <= 96 * 1024, "conv_wgrad_direct: image too wide");
+  static bool attr = false;
+  if (!attr) {
+    WAP_CUDA_TRY(cudaFuncSetAttribute(wgrad_direct_3x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    attr = true;
+  }
+  wgrad_direct_3x3_kernel<<<(unsigned)nblk, 256, smem, STREAM(stream)>>>(x, xl, dy, dyl, padding, work);
+  WAP_LAUNCH_CHECK();
+  const int warps = 27 * dyl.C;
+  wgrad_direct_final_kernel<<<(warps * 32 + 255) / 256, 256, 0, STREAM(stream)>>>(work, (int)nblk, dyl.C, dw, ldw);
+  WAP_LAUNCH_CHECK();
+  g_wap_launches.fetch_add(2, std::memory_order_relaxed);
+  return WAP_OK;
+}
+
 extern "C" int wap_conv_direct(const float* x, wap_layout_t xl, const float* w, int k, int padding, int ldw,
                                const float* bias, int relu, float* y, wap_layout_t yl, uint32_t* mbits,
                                int64_t mbits_ld, void* stream) {

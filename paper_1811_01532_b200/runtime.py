@@ -1164,11 +1164,23 @@ class Program:
             self._gemm(n.id, kk * kk * ci, co, x.rows, a, bo, dw)
         else:
             if self.strategy[conv] == "direct":
-                # the forward never built columns: im2col here, on the weight-gradient stream
                 cn = self.node(conv)
                 x_in = self._in(cn, cn.inputs[0])
                 s_, p_ = conv_geometry(cn, kk)
                 _, ho, wo, _ = self.dims(conv)
+                if (kk == 3 and s_ == 1 and p_ == 1 and ci == 3 and x_in.ld == 4 and (ho, wo) == tuple(x_in.dims[1:3])
+                        and os.environ.get("WAP_WGRAD_DIRECT", "0") == "1"):
+                    # 3-channel first layer: CUDA-core direct weight gradient, no im2col and no
+                    # M = 27 GEMM (csrc/ops.cu wgrad_direct_3x3_kernel). Opt-in: measured r02 on
+                    # VGG-16 conv1_1, 0.47 ms vs 0.34 ms for im2col + the tcgen05 GEMM
+                    work = self.torch.empty(int(self.L.wap_conv_wgrad_direct_work_floats(dy.layout())),
+                                            dtype=self.torch.float32, device=self.device)
+                    self._emit(n.id, self.L.wap_conv_wgrad_direct,
+                               (x_in.ptr, x_in.layout(), dy.ptr, dy.layout(), kk, p_, dw.ptr, dw.ld,
+                                work.data_ptr()), "direct weight gradient (3-channel first layer)",
+                               keep=[work], alg_bytes=self._nbytes(x_in, dy, dw))
+                    return
+                # the forward never built columns: im2col here, on the weight-gradient stream
                 K = kk * kk * ci
                 ldcol = _ceil4(K)
                 colb = self.torch.empty(dy.rows * ldcol, dtype=self.torch.float32, device=self.device)

@@ -215,3 +215,31 @@ def test_lrn_maxpool_fwd_fused_matches_unfused(cuda, B, H, C, win, pad):
     N.check(L.wap_lrn_maxpool_fwd(x.data_ptr(), xl, 5, a, beta, k, win, s, y2.data_ptr(), yl, a2.data_ptr(), None))
     torch.cuda.synchronize()
     assert torch.equal(y1, y2) and torch.equal(a1, a2)
+
+
+@pytest.mark.parametrize("B,H,W,pad", [(2, 33, 30, 1), (3, 9, 17, 2), (1, 6, 5, 0)])
+def test_conv_wgrad_direct_3x3_c3(cuda, B, H, W, pad):
+    """First-layer direct weight gradient (wap_conv_wgrad_direct: 3x3 same, C=3, dy on a
+    padded grid with a trailing halo) against torch fp64, and run-to-run bitwise equal."""
+    L = N.lib()
+    Co = 64
+    g = torch.Generator(device="cuda").manual_seed(43)
+    x = torch.zeros(B, H, W, 4, device=cuda)
+    x[..., :3] = torch.randn(B, H, W, 3, device=cuda, generator=g)
+    dy = torch.zeros(B, H + pad, W + pad, Co, device=cuda)
+    dy[:, :H, :W] = torch.randn(B, H, W, Co, device=cuda, generator=g)
+    xl = N.wap_layout_t(B, H, W, 3, 0, 4)
+    dl = N.wap_layout_t(B, H, W, Co, pad, Co)
+    work = torch.empty(int(L.wap_conv_wgrad_direct_work_floats(dl)), device=cuda)
+    outs = []
+    for _ in range(2):
+        dw = torch.full((27, Co), float("nan"), device=cuda)
+        N.check(L.wap_conv_wgrad_direct(x.data_ptr(), xl, dy.data_ptr(), dl, 3, 1, dw.data_ptr(), Co,
+                                        work.data_ptr(), None))
+        torch.cuda.synchronize()
+        outs.append(dw)
+    assert torch.equal(outs[0], outs[1])
+    xd = x[..., :3].double().permute(0, 3, 1, 2)
+    ref = torch.nn.grad.conv2d_weight(xd, (Co, 3, 3, 3), dy[:, :H, :W].double().permute(0, 3, 1, 2), padding=1)
+    ref = ref.permute(2, 3, 1, 0).reshape(27, Co)
+    assert ((outs[0].double() - ref).abs().max() / ref.abs().max()).item() < 1e-6
