@@ -1662,7 +1662,6 @@ __global__ void __launch_bounds__(256) wgrad_direct_3x3_kernel(const float* __re
     if (cc < Co) {
       // pixels w = g, g + 4, ... of each row; the dy loads of 4 pixels are issued together
       // (one round trip per 4 pixels instead of one per pixel)
-      const int64_t drow = (int64_t)(dl.W + dl.pad) * dl.ld;
       for (int r = 0; r < nr; ++r) {
         const float* dyr = dy + lidx(dl, b, h0 + r, 0, cc);
         const float4* xr = xs + r * W2;
@@ -1685,7 +1684,6 @@ __global__ void __launch_bounds__(256) wgrad_direct_3x3_kernel(const float* __re
             }
           }
         }
-        (void)drow;
       }
     }
     // sum the 4 pixel groups in order through shared memory (after the staged rows)
