@@ -708,6 +708,7 @@ class Program:
         stream = torch.cuda.current_stream(self.device)
         s = N.stream_ptr()
         free = os.environ.get("WAP_AUTOTUNE_FREE") == "1"
+        reps = int(os.environ.get("WAP_AUTOTUNE_REPS", reps))  # tools/tune_plans.py times longer
         self.tuned_plans: dict[str, dict] = {}
         for st in self.steps + self.update_steps:
             if not isinstance(st, _GemmStep):

@@ -19,6 +19,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 os.environ["WAP_AUTOTUNE_FREE"] = "1"
 os.environ["WAP_AUTOTUNE"] = "1"
+os.environ.setdefault("WAP_AUTOTUNE_REPS", "12")  # 12 timed launches per candidate (3 by default at run time)
 
 
 def main():
