@@ -161,7 +161,6 @@ struct Cfg {
   // PREC 3 smem stage: [A raw] | B raw | B small   (PAIR2: [A raw] | P | Q | R)
   static constexpr int B_REGION = PAIR2 ? 160 * 128 : 2 * B_BYTES;
   static constexpr int STAGE_BYTES = PREC == 3 ? (A_OFF + B_REGION) : (A_BYTES + B_BYTES);
-  // two accumulators (epilogue overlap) only if >= 4 A stages still fit in TMEM
   // PAIR (3xTF32, N = 64, one CTA): a tcgen05 MMA with N <= 64 costs about as much as
   // N = 108 (tools/mma_probe.cu: ~54 cycles vs 32 at full rate), so big*big and
   // big*small run as ONE N = 128 MMA over the contiguous [B_raw | B_small] rows of the
@@ -180,16 +179,18 @@ struct Cfg {
   // (three: d_conv2_w 0.30 -> 0.37 ms).
   static constexpr int SG = PAIR ? (WAP_PAIR_SG3 ? 3 : ((!WIN && WAP_PAIR_ONE_GROUP) ? 1 : kSplitGroups))
                                  : ((PREC == 3 && BN <= 128) ? WAP_SG_NARROW : kSplitGroups);
-  // halo-window pair kernels keep two groups but take an ODD ring of 3 A slots (the groups
-  // then also observe each other's steps, see EVEN): two accumulators + S + 3 x 64 columns
+  // (off, it hung a full-size d_pool1) halo-window pair kernels with an ODD ring of 3 A
+  // slots, the groups observing each other's steps (see EVEN); the default gives them an
+  // even ring of 2 slots (WAP_PAIR_WIN_MIN_SLOTS) and two accumulators + S instead
   static constexpr bool ODD_PAIR = PAIR && WIN && WAP_PAIR_ODD_RING;
+  // fewest A slots that must fit next to two accumulators + S (else: one accumulator)
   static constexpr int MIN_SLOTS =
       (SG == 1 || ODD_PAIR || (PAIR && SG == 3)) ? 3 : ((PAIR && WIN) ? WAP_PAIR_WIN_MIN_SLOTS : WAP_MIN_A_SLOTS);
   // SACC: two-half accumulators (big*big | small products); PAIR always has two halves
   // raw A from shared memory except for the single-CTA N = 64 pair kernels, where the
   // N = 128 SS MMA (A + all of [B | B_small] from this CTA's shared memory, ~128 B/clk)
   // measured slower than the TS form (tools/gpurun/r2_exp1.sh, r02); the TS form keeps
-  // 64-column A slots, so those kernels hold one accumulator buffer next to S
+  // 64-column A slots (3 or 2 of them next to two accumulators + S, see SG / MIN_SLOTS)
   static constexpr bool A_SS = WAP_A_SS && PREC == 3 && !(CG == 1 && BN == 64 && !WAP_PAIR_SS);
   static constexpr bool SACC = PREC == 3 && !PAIR && WAP_SPLIT_ACC && !A_SS;
   static constexpr bool HALVES = PAIR || PAIR2 || SACC;             // accumulator has two halves to add
